@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the PROFusion tracking-and-fusion hot path on B200 (BASELINE.json metric:
+particle-point TSDF evals/s; ms per 640x480 frame, track + integrate).
+
+One step = one frame of BASELINE config 3 ("Q"): track the 640x480 depth frame (160x120 strided
+points, K = 2048 particles per GPU, 10 iterations, init = GT (+) U+-5 deg/+-5 cm standing in for the
+regression network) against a 512^3 @ 1 cm fp32 TSDF, then integrate the frame at the tracked
+pose.  The TSDF is first built by integrating `--map-frames` frames of the trajectory at GT.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our CUDA path (libpft.so)
+  python bench.py --impl reference [...]                   # the fp64 CPU oracle on a bounded sample
+
+Multi-GPU (torchrun, one rank per GPU): particles are sharded (K = 2048 * N in total, weak
+scaling), the volume is replicated, per-particle results are all-gathered over NCCL each
+iteration.  Timing: CUDA events around each step on the launching stream, L2 flushed (256 MiB
+write) between steps outside the events, max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_PER_GPU = 2048
+ITERS = 10
+BYTES_PER_EVAL = 32          # 8 trilinear corners x fp32 value
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--map-frames", type=int, default=8)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------- workload
+def make_workload(args, n_steps, world):
+    from synth.configs import Sequence, init_noise
+    from synth.scene import Intrinsics  # noqa: F401
+    nf = args.map_frames + n_steps
+    seq = Sequence("Q", seed=args.seed, n_frames=max(nf, 48), K=K_PER_GPU * world, iters=ITERS)
+    map_depth = [seq.depth(t) for t in range(args.map_frames)]
+    steps = []
+    for i in range(n_steps):
+        t = args.map_frames + i
+        steps.append(dict(t=t, depth=seq.depth(t), T_init=init_noise(args.seed, t, seq.gt[t], 5.0, 5.0)))
+    return seq, map_depth, steps
+
+
+def strided_valid(depth, stride, max_depth=8.0):
+    d = depth[::stride, ::stride].astype(np.float64) * 0.001
+    return int(((depth[::stride, ::stride] > 0) & (d < max_depth)).sum())
+
+
+# ---------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.lines, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- our path
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2509_24236_b200 as pft
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    seq, map_depth, steps_in = make_workload(args, args.warmup + args.steps, world)
+    desc, intr, params = seq.desc, seq.intr, seq.params
+    K = K_PER_GPU * world
+
+    vol = pft.Volume(desc, dev)
+    vol.reset()
+    for t, d in enumerate(map_depth):
+        vol.integrate(torch.from_numpy(d).to(dev), intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
+    if world > 1:
+        vol.comm_init()
+    pst = torch.from_numpy(seq.pst).to(dev)
+    depth_dev = [torch.from_numpy(s["depth"]).to(dev) for s in steps_in]
+    tinit_dev = [torch.from_numpy(s["T_init"]).to(dev) for s in steps_in]
+    n_valid = [strided_valid(s["depth"], params.stride) for s in steps_in]
+    evals = [K * n * ITERS for n in n_valid]
+    out = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(K, dtype=torch.float64, device=dev),
+               n=torch.empty(K, dtype=torch.int32, device=dev),
+               trace=torch.zeros(ITERS, pft.TRACE_DOUBLES, dtype=torch.float64, device=dev))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(i, depth, T_init):
+        vol.track(depth, intr, T_init, pst, params, out=out)
+        vol.integrate(depth, intr, out["T"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i, depth_dev[i], tinit_dev[i])
+    barrier()
+
+    # ---- device-resident timed region
+    idx = list(range(args.warmup, args.warmup + args.steps))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
+    with Clocks(local) as clk:
+        barrier()
+        pft.profile_start()
+        l0 = pft.launch_count()
+        for j, i in enumerate(idx):
+            flush.zero_()
+            ev[j][0].record(stream)
+            step(i, depth_dev[i], tinit_dev[i])
+            ev[j][1].record(stream)
+        barrier()
+        launches = pft.launch_count() - l0
+        prof = pft.profile_stop()
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    n_chk = int(out["trace"][-1, 21].item())
+    assert n_chk == n_valid[idx[-1]], (n_chk, n_valid[idx[-1]])
+    t_ms = sum(per_step)
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    tot_evals = sum(evals[i] for i in idx)
+    value = tot_evals / (t_max * 1e-3)
+
+    # ---- end-to-end through the public API with host buffers
+    host_depth = [torch.from_numpy(s["depth"]).pin_memory() for s in steps_in]
+    host_tinit = [torch.from_numpy(s["T_init"]).pin_memory() for s in steps_in]
+    host_T = torch.empty(3, 4, dtype=torch.float64).pin_memory()
+    d_buf = torch.empty_like(depth_dev[0])
+    t_buf = torch.empty_like(tinit_dev[0])
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
+    barrier()
+    for j, i in enumerate(idx):
+        flush.zero_()
+        ev2[j][0].record(stream)
+        d_buf.copy_(host_depth[i], non_blocking=True)
+        t_buf.copy_(host_tinit[i], non_blocking=True)
+        step(i, d_buf, t_buf)
+        host_T.copy_(out["T"], non_blocking=True)
+        ev2[j][1].record(stream)
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ev2)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    h2d = host_depth[0].numel() * 2 + 96
+    d2h = 96
+
+    # ---- roofline of the dominant kernel (k_particle_eval)
+    eval_ms, eval_n = prof["eval"]
+    evals_per_launch = K_PER_GPU * statistics.mean(n_valid[i] for i in idx)
+    avg_launch_s = eval_ms / eval_n * 1e-3
+    achieved = evals_per_launch * BYTES_PER_EVAL / avg_launch_s / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "eval_traffic.json")
+    if os.path.exists(tf):
+        tj = json.load(open(tf))
+        traffic = tj.get("dram_bytes_per_eval", 0) * evals_per_launch
+
+    res = {
+        "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
+        "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 transform/decisions, f32 TSDF + lerp, int64 fixed-point sums",
+        "data": "synthetic (seeded box room + shaky trajectory, BASELINE config 3)",
+        "config": {"workload": "Q: 640x480 frame, 160x120 points, K=2048/GPU, 10 iters, 512^3 @1cm fp32 TSDF, "
+                               "track + integrate", "particles": K, "points_per_frame": statistics.mean(n_valid),
+                   "iters": ITERS, "volume": "512^3 fp32", "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"particles sharded x{world}, volume replicated"},
+        "frame_ms": {"median": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
+                     "max": max(per_step)},
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "e2e": {"value": tot_evals / (e2e_ms * 1e-3), "unit": "evals/s", "ms_per_step": e2e_ms / args.steps,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_particle_eval",
+                     "basis": f"{BYTES_PER_EVAL} B logical gather/eval x {evals_per_launch:.0f} evals/launch; "
+                              "gathers are L2/L1-resident (DESIGN.md §7)",
+                     "evals_per_s_kernel": evals_per_launch / avg_launch_s},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args, seq, map_depth, steps_in[idx[0]])
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    vol.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- oracle arms
+def oracle_map(seq, map_depth):
+    import oracle
+    ov = oracle.OracleVolume(seq.desc)
+    for t, d in enumerate(map_depth):
+        ov.integrate(d, seq.intr, seq.gt[t])
+    return ov
+
+
+def cores():
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(args, seq, map_depth, s, K_sample=512):
+    """The oracle as it stands, on this host's cores: one RO iteration of K_sample particles on the
+    frame (a bounded sample of the step), reported in evals/s."""
+    from synth.configs import TrackParams
+    ov = oracle_map(seq, map_depth)
+    prm = TrackParams(iters=1, stride=4)
+    t0 = time.perf_counter()
+    r = ov.track(s["depth"], seq.intr, s["T_init"], seq.pst[:K_sample], prm, nthreads=cores())
+    dt = time.perf_counter() - t0
+    ev = K_sample * r["N"] * 1 + 2 * r["N"]
+    return {"value": ev / dt, "unit": "evals/s", "cores": cores(), "kind": "oracle",
+            "sample": f"1 RO iteration, {K_sample} of {seq.K} particles, {r['N']} points, 512^3 fp32 map "
+                      f"({len(map_depth)} frames fused by the oracle); {dt:.2f} s"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth.configs import TrackParams
+    seq, map_depth, steps_in = make_workload(args, args.warmup + args.steps, 1)
+    ov = oracle_map(seq, map_depth)
+    K_sample = 256
+    prm = TrackParams(iters=1, stride=4)
+    per, evs = [], []
+    for i, s in enumerate(steps_in):
+        t0 = time.perf_counter()
+        r = ov.track(s["depth"], seq.intr, s["T_init"], seq.pst[:K_sample], prm, nthreads=cores())
+        ov.integrate(s["depth"], seq.intr, r["T"], nthreads=cores())
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            per.append(dt)
+            evs.append(K_sample * r["N"])
+    value = sum(evs) / sum(per)
+    res = {"impl": "reference",
+           "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
+           "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * sum(per) / len(per), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded box room + shaky trajectory, config 3)",
+           "config": {"workload": "Q: 640x480 frame, 160x120 points, 512^3 @1cm fp32 TSDF, track + integrate; "
+                                  f"oracle sample: {K_sample} particles x 1 iteration per step"},
+           "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores(), "kind": "oracle",
+                            "sample": f"per step: 1 RO iteration of {K_sample} particles + full fusion sweep"},
+           "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,205 @@
+// abi.cu — error reporting, shared validation, volume destruction and the NCCL plumbing of
+// the multi-GPU path (north_star: particles sharded across the GPUs of one box, volume
+// replicated, per-particle fitness all-gathered over NVLink).
+//
+// NCCL is loaded with dlopen at pft_comm_init time ("libnccl.so.2", normally already mapped
+// by torch), so the library loads and runs single-GPU without NCCL on the link line.
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <nccl.h>
+
+#include "pft_internal.cuh"
+
+namespace pft {
+
+static thread_local char g_err[512] = "";
+
+pft_status fail(pft_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+pft_status cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return PFT_OK;
+  return fail(PFT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+pft_status check_intrinsics(const pft_intrinsics* K) {
+  if (!K) return fail(PFT_ERR_INVALID_ARG, "intrinsics is NULL");
+  if (!(K->fx > 0.0) || !(K->fy > 0.0)) return fail(PFT_ERR_INVALID_ARG, "fx, fy must be > 0 (SPEC.md:149)");
+  if (K->width < 1 || K->height < 1 || K->width > 16384 || K->height > 16384)
+    return fail(PFT_ERR_INVALID_ARG, "bad image size %dx%d", K->width, K->height);
+  if (!(K->depth_unit_m > 0.0)) return fail(PFT_ERR_INVALID_ARG, "depth_unit_m must be > 0");
+  if (!(K->cx == K->cx) || !(K->cy == K->cy)) return fail(PFT_ERR_INVALID_ARG, "cx, cy must be finite");
+  return PFT_OK;
+}
+
+// ------------------------------------------------------------------ instrumentation
+
+static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<bool> g_prof_on{false};
+struct ProfRec { int cls; cudaEvent_t a, b; };
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;       // recorded this session
+static std::vector<cudaEvent_t> g_pool;   // reusable events
+static thread_local cudaEvent_t t_open = nullptr;
+constexpr size_t kProfMax = 65536;
+
+static cudaEvent_t ev_get() {
+  if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(int cls, cudaStream_t st) {
+  (void)cls;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g_prof.size() >= kProfMax) return;
+  t_open = ev_get();
+  cudaEventRecord(t_open, st);
+}
+
+void prof_end(int cls, cudaStream_t st) {
+  if (!g_prof_on.load(std::memory_order_relaxed) || !t_open) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t b = ev_get();
+  cudaEventRecord(b, st);
+  g_prof.push_back(ProfRec{cls, t_open, b});
+  t_open = nullptr;
+}
+
+// ------------------------------------------------------------------ NCCL via dlopen
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommGetAsyncError) asyncErr = nullptr;
+};
+
+static Nccl* nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+      n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+      n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+      n.errStr = (decltype(n.errStr))dlsym(h, "ncclGetErrorString");
+      n.asyncErr = (decltype(n.asyncErr))dlsym(h, "ncclCommGetAsyncError");
+      if (n.getUniqueId && n.commInitRank && n.commDestroy && n.allGather && n.errStr) n.h = h;
+    }
+  }
+  return n.h ? &n : nullptr;
+}
+
+pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st) {
+  Nccl* n = nccl();
+  if (!n || !vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator not initialised");
+  prof_begin(PFT_PROF_COMM, st);
+  ncclResult_t r = n->allGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)vol->nccl_comm, st);
+  prof_end(PFT_PROF_COMM, st);
+  if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclAllGather: %s", n->errStr(r));
+  return PFT_OK;
+}
+
+}  // namespace pft
+
+using namespace pft;
+
+extern "C" {
+
+const char* pft_last_error(void) { return g_err; }
+
+int32_t pft_abi_version(void) { return PFT_ABI_VERSION; }
+
+uint64_t pft_launch_count(void) { return g_launches.load(); }
+
+pft_status pft_profile_start(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+  g_prof.clear();
+  g_prof_on.store(true);
+  return PFT_OK;
+}
+
+pft_status pft_profile_stop(double* ms_out, int64_t* launches_out) {
+  g_prof_on.store(false);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double ms[PFT_PROF_CLASSES] = {0};
+  int64_t cnt[PFT_PROF_CLASSES] = {0};
+  pft_status s = PFT_OK;
+  for (auto& r : g_prof) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) { s = cuda_check("profile_stop"); break; }
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cls >= 0 && r.cls < PFT_PROF_CLASSES) { ms[r.cls] += t; cnt[r.cls] += 1; }
+  }
+  for (auto& r : g_prof) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+  g_prof.clear();
+  for (int i = 0; i < PFT_PROF_CLASSES; ++i) {
+    if (ms_out) ms_out[i] = ms[i];
+    if (launches_out) launches_out[i] = cnt[i];
+  }
+  return s;
+}
+
+pft_status pft_volume_destroy(pft_volume* vol) {
+  if (!vol) return PFT_OK;
+  if (vol->nccl_comm) {
+    Nccl* n = nccl();
+    if (n) n->commDestroy((ncclComm_t)vol->nccl_comm);
+  }
+  delete vol;
+  return PFT_OK;
+}
+
+pft_status pft_comm_get_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(PFT_ERR_INVALID_ARG, "id_out is NULL");
+  Nccl* n = nccl();
+  if (!n) return fail(PFT_ERR_NCCL, "libnccl.so.2 not loadable: %s", dlerror());
+  ncclUniqueId id;
+  ncclResult_t r = n->getUniqueId(&id);
+  if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclGetUniqueId: %s", n->errStr(r));
+  memcpy(id_out, id.internal, 128);
+  return PFT_OK;
+}
+
+pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks, int32_t rank) {
+  if (!vol || !id) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PFT_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+  if (vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator already initialised");
+  if (nranks == 1) { vol->nranks = 1; vol->rank = 0; return PFT_OK; }
+  Nccl* n = nccl();
+  if (!n) return fail(PFT_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, 128);
+  ncclComm_t comm;
+  ncclResult_t r = n->commInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclCommInitRank: %s", n->errStr(r));
+  vol->nccl_comm = comm;
+  vol->nranks = nranks;
+  vol->rank = rank;
+  return PFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,248 @@
+// integrate.cu — KinectFusion TSDF fusion of one depth frame ("The fusion process
+// remains the same as KinectFusion"; reading L22/L23 in DESIGN.md §3).
+//
+// Per voxel, in this exact fp64 operation order (no FMA contraction, IEEE division), so the
+// stored bits equal a plain fp64 evaluation of the same formulas:
+//   g_w = o + s*(i + 1/2);  p_c = R^T (g_w - t);  skip unless z_c > 0;
+//   u = fx*x/z + cx, v = fy*y/z + cy;  pixel = (floor(u + 1/2), floor(v + 1/2)) inside and valid;
+//   sdf = d - z_c;  skip unless sdf > -tau;  v_new = min(1, sdf/tau);
+//   V' = (V W + v_new)/(W + 1), W' = min(W + 1, W_max), each rounded once (RNE) to storage.
+//
+// B200 design: the update set of a frame is the camera frustum up to the
+// surface + tau, a few % of a room-scale grid.  A per-brick cull (conservative, fp32 with
+// margins) compacts the 4^3 bricks that can contain an updated voxel; the fusion kernel then
+// sweeps only those bricks, 64 consecutive elements (one brick = 2 x 128 B lines per array
+// at fp32) per pair of warps, fully coalesced.  The full sweep is kept for verification.
+#include "pft_internal.cuh"
+
+namespace pft {
+
+struct Intr {
+  double fx, fy, cx, cy, unit;
+  int W, H;
+};
+
+template <typename T> __device__ __forceinline__ double to_double(T x);
+template <> __device__ __forceinline__ double to_double<float>(float x) { return (double)x; }
+template <> __device__ __forceinline__ double to_double<__half>(__half x) { return (double)__half2float(x); }
+template <typename T> __device__ __forceinline__ T store_rn(double x);
+template <> __device__ __forceinline__ float store_rn<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ __half store_rn<__half>(double x) { return __double2half(x); }
+
+template <typename T>
+__device__ __forceinline__ void fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
+                                           const double* T_, int i, int j, int k, T* __restrict__ V,
+                                           T* __restrict__ W, uint32_t o) {
+  const double gw0 = __dadd_rn(g.ox, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
+  const double gw1 = __dadd_rn(g.oy, __dmul_rn(g.voxel, __dadd_rn((double)j, 0.5)));
+  const double gw2 = __dadd_rn(g.oz, __dmul_rn(g.voxel, __dadd_rn((double)k, 0.5)));
+  const double d0 = __dsub_rn(gw0, T_[3]), d1 = __dsub_rn(gw1, T_[7]), d2 = __dsub_rn(gw2, T_[11]);
+  const double z = __dadd_rn(__dadd_rn(__dmul_rn(T_[2], d0), __dmul_rn(T_[6], d1)), __dmul_rn(T_[10], d2));
+  if (!(z > 0.0)) return;
+  const double x = __dadd_rn(__dadd_rn(__dmul_rn(T_[0], d0), __dmul_rn(T_[4], d1)), __dmul_rn(T_[8], d2));
+  const double y = __dadd_rn(__dadd_rn(__dmul_rn(T_[1], d0), __dmul_rn(T_[5], d1)), __dmul_rn(T_[9], d2));
+  const double u = __dadd_rn(__ddiv_rn(__dmul_rn(K.fx, x), z), K.cx);
+  const double uf = floor(__dadd_rn(u, 0.5));
+  if (!(uf >= 0.0 && uf < (double)K.W)) return;
+  const double v = __dadd_rn(__ddiv_rn(__dmul_rn(K.fy, y), z), K.cy);
+  const double vf = floor(__dadd_rn(v, 0.5));
+  if (!(vf >= 0.0 && vf < (double)K.H)) return;
+  const uint16_t raw = __ldg(depth + (size_t)vf * K.W + (size_t)uf);
+  const double d = __dmul_rn((double)raw, K.unit);
+  if (raw == 0 || !(d < g.max_depth)) return;
+  const double sdf = __dsub_rn(d, z);
+  if (!(sdf > -g.trunc)) return;
+  double vnew = __ddiv_rn(sdf, g.trunc);
+  if (vnew > 1.0) vnew = 1.0;
+  const double Vo = to_double<T>(V[o]), Wo = to_double<T>(W[o]);
+  const double Wp = __dadd_rn(Wo, 1.0);
+  const double Vn = __ddiv_rn(__dadd_rn(__dmul_rn(Vo, Wo), vnew), Wp);
+  const double Wn = Wp > g.max_weight ? g.max_weight : Wp;
+  V[o] = store_rn<T>(Vn);
+  W[o] = store_rn<T>(Wn);
+}
+
+// Full sweep: one thread per brick element (the verification path).
+template <typename T>
+__global__ __launch_bounds__(256) void k_integrate_sweep(Geom g, Intr K, const uint16_t* __restrict__ depth,
+                                                         const double* __restrict__ Tdev, T* __restrict__ V,
+                                                         T* __restrict__ W, size_t nelem) {
+  __shared__ double sT[12];
+  if (threadIdx.x < 12) sT[threadIdx.x] = Tdev[threadIdx.x];
+  __syncthreads();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < nelem; e += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)(e >> 6), w = (uint32_t)(e & 63);
+    const int bx = (int)(b % (uint32_t)g.nbx);
+    const uint32_t r = b / (uint32_t)g.nbx;
+    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+    const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
+    if (i >= g.nx || j >= g.ny || k >= g.nz) continue;
+    fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, (uint32_t)e);
+  }
+}
+
+// ---- culling ---------------------------------------------------------------------------------
+constexpr int kTile = 8;  // depth tiles of 8x8 pixels
+
+// Per tile: the maximum valid raw depth (0 if the tile has no valid pixel).  Validity is the
+// exact fp64 test of O1 (raw > 0 and raw*unit < max_depth).
+__global__ void k_depth_tiles(Intr K, double max_depth, const uint16_t* __restrict__ depth, uint32_t* __restrict__ tiles,
+                              int ntx, int nty) {
+  const int t = blockIdx.x * blockDim.y + threadIdx.y;  // one warp per tile
+  if (t >= ntx * nty) return;
+  const int tx = t % ntx, ty = t / ntx;
+  uint32_t m = 0;
+  for (int p = threadIdx.x; p < kTile * kTile; p += 32) {
+    const int u = tx * kTile + (p & 7), v = ty * kTile + (p >> 3);
+    if (u < K.W && v < K.H) {
+      const uint16_t raw = depth[(size_t)v * K.W + u];
+      if (raw != 0 && __dmul_rn((double)raw, K.unit) < max_depth) m = max(m, (uint32_t)raw);
+    }
+  }
+  for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if (threadIdx.x == 0) tiles[t] = m;
+}
+
+// One thread per brick.  A brick is dropped only when no voxel centre in it can pass the
+// voxel-level tests: all z_c <= 0, or its projection misses the image, or every pixel it can
+// project to is invalid / has d + tau <= z_c.  Bounds use the bounding sphere of the brick's
+// voxel centres with margins (1 mm, 2 px) far above fp32 rounding at room scale.
+__global__ void k_cull(Geom g, Intr K, const double* __restrict__ Tdev, const uint32_t* __restrict__ tiles,
+                       int ntx, int nty, uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
+  const uint32_t nb = (uint32_t)g.nbx * g.nby * g.nbz;
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (b < nb) {
+    const int bx = (int)(b % (uint32_t)g.nbx);
+    const uint32_t r = b / (uint32_t)g.nbx;
+    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+    // centre of the brick's voxel-centre box and its radius
+    const float vox = (float)g.voxel;
+    const float cwx = (float)(g.ox + g.voxel * (4.0 * bx + 2.0)) - (float)Tdev[3];
+    const float cwy = (float)(g.oy + g.voxel * (4.0 * by + 2.0)) - (float)Tdev[7];
+    const float cwz = (float)(g.oz + g.voxel * (4.0 * bz + 2.0)) - (float)Tdev[11];
+    const float rad = 1.5f * 1.7320508f * vox + 1e-3f;
+    const float x = (float)Tdev[0] * cwx + (float)Tdev[4] * cwy + (float)Tdev[8] * cwz;
+    const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
+    const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
+    if (z + rad > 0.f) {
+      if (z - rad <= 1e-3f) {
+        keep = true;  // straddles the camera plane: no projection bound
+      } else {
+        const float zn = z - rad, zf = z + rad;
+        const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
+        const float u0 = fx * fminf((x - rad) / zn, (x - rad) / zf) + cx - 2.f;
+        const float u1 = fx * fmaxf((x + rad) / zn, (x + rad) / zf) + cx + 2.f;
+        const float v0 = fy * fminf((y - rad) / zn, (y - rad) / zf) + cy - 2.f;
+        const float v1 = fy * fmaxf((y + rad) / zn, (y + rad) / zf) + cy + 2.f;
+        if (u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H) {
+          const int pu0 = max(0, (int)floorf(u0 + 0.5f)), pu1 = min(K.W - 1, (int)floorf(u1 + 0.5f));
+          const int pv0 = max(0, (int)floorf(v0 + 0.5f)), pv1 = min(K.H - 1, (int)floorf(v1 + 0.5f));
+          const int t0x = pu0 / kTile, t1x = pu1 / kTile, t0y = pv0 / kTile, t1y = pv1 / kTile;
+          if ((t1x - t0x + 1) * (t1y - t0y + 1) > 64) {
+            keep = true;  // very close brick: do not bother bounding the depth
+          } else {
+            uint32_t m = 0;
+            for (int ty = t0y; ty <= t1y; ++ty)
+              for (int tx = t0x; tx <= t1x; ++tx) m = max(m, __ldg(tiles + ty * ntx + tx));
+            if (m > 0) {
+              const float dmax = (float)((double)m * K.unit);
+              keep = zn - 1e-3f < dmax + (float)g.trunc;
+            }
+          }
+        }
+      }
+    }
+  }
+  // warp-aggregated append
+  const unsigned ball = __ballot_sync(0xffffffffu, keep);
+  if (ball) {
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(count, (uint32_t)__popc(ball));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) list[base + __popc(ball & ((1u << lane) - 1))] = b;
+  }
+}
+
+// Sweep of the compacted bricks: 4 bricks per 256-thread CTA, grid-stride over the list.
+template <typename T>
+__global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const uint16_t* __restrict__ depth,
+                                                        const double* __restrict__ Tdev, const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count, T* __restrict__ V,
+                                                        T* __restrict__ W) {
+  __shared__ double sT[12];
+  if (threadIdx.x < 12) sT[threadIdx.x] = Tdev[threadIdx.x];
+  __syncthreads();
+  const uint32_t n = *count;
+  const uint32_t w = threadIdx.x & 63;
+  for (uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6); li < n; li += gridDim.x * 4) {
+    const uint32_t b = list[li];
+    const int bx = (int)(b % (uint32_t)g.nbx);
+    const uint32_t r = b / (uint32_t)g.nbx;
+    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+    const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
+    if (i >= g.nx || j >= g.ny || k >= g.nz) continue;
+    fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, b * 64u + w);
+  }
+}
+
+pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intrinsics* Kp, const double* T,
+                          int full_sweep, cudaStream_t st) {
+  Intr K{Kp->fx, Kp->fy, Kp->cx, Kp->cy, Kp->depth_unit_m, Kp->width, Kp->height};
+  const Geom& g = vol->g;
+  const int ntx = (K.W + kTile - 1) / kTile, nty = (K.H + kTile - 1) / kTile;
+  if ((size_t)ntx * nty * 4 > vol->L.tiles_bytes) full_sweep = 1;
+  if (full_sweep) {
+    size_t n = vol->L.elems;
+    size_t blocks = (n + 255) / 256;
+    int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
+    if (vol->esize == 4)
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<float><<<grid, 256, 0, st>>>(g, K, depth, T, (float*)(vol->base + vol->L.v_off),
+                                                     (float*)(vol->base + vol->L.w_off), n));
+    else
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<__half><<<grid, 256, 0, st>>>(g, K, depth, T, (__half*)(vol->base + vol->L.v_off),
+                                                      (__half*)(vol->base + vol->L.w_off), n));
+    return cuda_check("integrate (full sweep)");
+  }
+  uint32_t* tiles = (uint32_t*)(vol->base + vol->L.tiles_off);
+  uint32_t* list = (uint32_t*)(vol->base + vol->L.list_off);
+  uint32_t* count = (uint32_t*)(vol->base + vol->L.scratch_off + 64);
+  cudaMemsetAsync(count, 0, 4, st);
+  {
+    dim3 blk(32, 8);
+    int nt = ntx * nty;
+    PFT_LAUNCH(PFT_PROF_CULL, st, k_depth_tiles<<<(nt + 7) / 8, blk, 0, st>>>(K, g.max_depth, depth, tiles, ntx, nty));
+  }
+  const uint32_t nb = (uint32_t)g.nbx * g.nby * g.nbz;
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull<<<(nb + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nty, list, count));
+  const int grid = 148 * 8;
+  if (vol->esize == 4)
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (float*)(vol->base + vol->L.v_off),
+                                                  (float*)(vol->base + vol->L.w_off)));
+  else
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (__half*)(vol->base + vol->L.v_off),
+                                                   (__half*)(vol->base + vol->L.w_off)));
+  return cuda_check("integrate");
+}
+
+}  // namespace pft
+
+using namespace pft;
+
+extern "C" {
+
+pft_status pft_integrate_ex(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K, const double* dev_T,
+                            int32_t flags, void* stream) {
+  if (!vol || !dev_depth || !dev_T) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  pft_status s = check_intrinsics(K);
+  if (s != PFT_OK) return s;
+  return integrate_impl(vol, dev_depth, K, dev_T, flags & 1, (cudaStream_t)stream);
+}
+
+pft_status pft_integrate(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K, const double* dev_T,
+                         void* stream) {
+  return pft_integrate_ex(vol, dev_depth, K, dev_T, 0, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// pft_internal.cuh — internal declarations shared by the libpft translation units.
+// Nothing here is part of the ABI (include/pft.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/pft.h"
+
+namespace pft {
+
+// ------------------------------------------------------------------ volume layout
+// TSDF storage is SoA (values, weights) in 4x4x4-voxel bricks: a brick is 64
+// consecutive elements, z-major inside (z*16 + y*4 + x), bricks x-fastest.  The element
+// offset of voxel (x,y,z) is separable: offx(x) + offy(y) + offz(z), so the 8 trilinear
+// corners cost 6 offset terms and 8 adds.
+constexpr int kBrick = 4;
+constexpr int kBrickVox = 64;
+
+struct Geom {
+  int nx, ny, nz;          // voxels
+  int nbx, nby, nbz;       // bricks
+  uint32_t sy, sz;         // brick-row / brick-slab strides in elements (64*nbx, 64*nbx*nby)
+  double voxel, ox, oy, oz;
+  double trunc, max_weight, max_depth;
+};
+
+__host__ __device__ __forceinline__ uint32_t offx(int x) { return ((uint32_t)(x >> 2) << 6) | (uint32_t)(x & 3); }
+__host__ __device__ __forceinline__ uint32_t offy(int y, uint32_t sy) { return (uint32_t)(y >> 2) * sy + ((uint32_t)(y & 3) << 2); }
+__host__ __device__ __forceinline__ uint32_t offz(int z, uint32_t sz) { return (uint32_t)(z >> 2) * sz + ((uint32_t)(z & 3) << 4); }
+
+// Byte layout of the caller-owned volume storage.
+struct VolLayout {
+  size_t scratch_off, scratch_bytes;  // checksum / counters
+  size_t v_off, w_off, elems;         // elems = nbx*nby*nbz*64 per array
+  size_t list_off, list_bytes;        // integration: active brick list (uint32 per brick)
+  size_t tiles_off, tiles_bytes;      // integration: per-tile depth max (float)
+  size_t total;
+};
+
+}  // namespace pft
+
+struct pft_volume {
+  pft_volume_desc desc;
+  pft::Geom g;
+  pft::VolLayout L;
+  size_t esize;     // 4 (fp32) or 2 (fp16)
+  char* base;
+  int device;
+  // multi-GPU
+  void* nccl_comm;
+  int nranks, rank;
+};
+
+namespace pft {
+
+// ------------------------------------------------------------------ tracking state / records
+// Per-particle accumulator, exchanged as-is by the all-gather (16 B).
+// S = sum over in-band points of |v| in fixed point (units of 2^-kFixBits), n = in-band count.
+struct PartRec {
+  unsigned long long S;
+  unsigned int n;
+  unsigned int pad;
+};
+constexpr int kFixBits = 29;  // per-thread partial sums of <= 7 terms in [0,1) fit in uint32
+
+// Device-resident state of one pft_track call (lives at the start of the workspace).
+struct TrackState {
+  double P[12];        // current pose P^(i)
+  double omega, v;     // current search size s^(i) (deg, cm)
+  double Ec;           // E(P) of the current pose
+  double Ebase;        // E of the pose the current iteration started from
+  unsigned long long Sc_acc;  // centre accumulators (zeroed after use)
+  unsigned int nc_acc;
+  unsigned int nc;     // in-band count of the current pose
+  int nA;              // |A| of the last update
+  int iter;            // iterations completed
+  int Nvalid;          // valid strided points
+  unsigned int ticket_upd, ticket_ctr;
+  int pad0;
+  double pad[8];
+};
+
+struct TrackLayout {
+  size_t state_off;
+  size_t pts_off;      // 3 * npad doubles (x, y, z SoA)
+  size_t acc_local_off, acc_full_off;
+  size_t part_off;     // update partials: nblk_upd * 8 doubles
+  size_t total;
+  int npad, ntx, nty, nr, nc;  // point slots, tiles, strided grid rows / cols
+  int kloc, kfull, nblk_upd;
+};
+
+}  // namespace pft
+
+namespace pft {
+// Error reporting (abi.cu): records a thread-local message and returns s.
+pft_status fail(pft_status s, const char* fmt, ...);
+// cudaGetLastError() after a launch sequence -> PFT_OK or PFT_ERR_CUDA with the message.
+pft_status cuda_check(const char* what);
+// Launch instrumentation (abi.cu): call prof_begin before and prof_end after each launch.
+void prof_begin(int cls, cudaStream_t st);
+void prof_end(int cls, cudaStream_t st);
+#define PFT_LAUNCH(cls, st, ...)        \
+  do {                                  \
+    ::pft::prof_begin((cls), (st));     \
+    __VA_ARGS__;                        \
+    ::pft::prof_end((cls), (st));       \
+  } while (0)
+// Validation helpers shared by the entry points.
+pft_status check_intrinsics(const pft_intrinsics* K);
+pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
+                        int32_t stride, int nranks, TrackLayout* L);
+}  // namespace pft

@@ -1,0 +1,688 @@
+// track.cu — randomized-optimisation tracking (§III-B) on the TSDF.
+//
+// Step map:
+//   k_track_init     a: state <- (T_init, s^(1)); zero accumulators
+//   k_backproject    a1/a2: uint16 depth -> strided fp64 points, 8x4-pixel tile order
+//   k_centre         a5: E(P) of the current pose (+ s-law a8 and the trace in its last block)
+//   k_particle_eval  a3/a4: candidate poses dP_k P built per CTA in smem; particle x point
+//                    tile, TSDF trilinear gathers from brick-ordered storage, per-warp
+//                    reductions (REDUX) -> per-CTA smem -> one global atomic per particle
+//   [ncclAllGather]  a6 (multi-GPU)
+//   k_update         a7: E_k, advantage set, quaternion/translation mean, pose update; the
+//                    last CTA to finish combines the per-CTA partials in a fixed order
+//
+// Numerics: every discrete decision (cell floor, bounds,
+// in-band, E_k < E_c) is made from fp64 transforms of fp64 points; lerps are fp32; sums are
+// fixed-point integers (2^-29) so per-particle totals are exact and independent of order,
+// CTA shape and sharding.
+#include <cmath>
+
+#include "pft_internal.cuh"
+
+namespace pft {
+
+constexpr int kThreads = 256;  // 8 warps
+constexpr int kPPT = 2;        // points per thread (one 8x4 tile per warp per p)
+constexpr int kPC = 32;        // particles per CTA chunk
+constexpr int kPointsPerCTA = kThreads * kPPT;
+constexpr double kFixScale = 536870912.0;            // 2^29
+constexpr double kFixInv = 1.0 / 536870912.0;        // 2^-29
+
+struct Pose12 { double m[12]; };  // folded: g = M p + c, rows [M00 M01 M02 c0 | ...]
+
+// ------------------------------------------------------------------ pose algebra (fp64)
+// Rodrigues (reading L9): dR = I + (sin th/th)[r]x + ((1-cos th)/th^2)[r]x^2, th < 1e-12: I + [r]x.
+__device__ __forceinline__ void rodrigues(const double r[3], double dR[9]) {
+  const double th = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  double A, B;
+  if (th < 1e-12) {
+    A = 1.0; B = 0.0;
+  } else {
+    double s, c;
+    sincos(th, &s, &c);
+    A = s / th;
+    B = (1.0 - c) / (th * th);
+  }
+  const double K[9] = {0.0, -r[2], r[1], r[2], 0.0, -r[0], -r[1], r[0], 0.0};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double k2 = K[3 * i + 0] * K[0 + j] + K[3 * i + 1] * K[3 + j] + K[3 * i + 2] * K[6 + j];
+      dR[3 * i + j] = (i == j ? 1.0 : 0.0) + A * K[3 * i + j] + B * k2;
+    }
+}
+
+// Unit quaternion (w,x,y,z) of rotation vector r (Hamilton, active): (cos th/2, r sin(th/2)/th).
+__device__ __forceinline__ void rotvec_quat(const double r[3], double q[4]) {
+  const double th = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (th < 1e-12) {
+    q[0] = 1.0; q[1] = r[0] * 0.5; q[2] = r[1] * 0.5; q[3] = r[2] * 0.5;
+  } else {
+    double s, c;
+    sincos(0.5 * th, &s, &c);
+    const double sh = s / th;
+    q[0] = c; q[1] = r[0] * sh; q[2] = r[1] * sh; q[3] = r[2] * sh;
+  }
+}
+
+__device__ __forceinline__ void quat_to_R(const double q[4], double R[9]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0] = 1.0 - 2.0 * (y * y + z * z); R[1] = 2.0 * (x * y - w * z);       R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);       R[4] = 1.0 - 2.0 * (x * x + z * z); R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);       R[7] = 2.0 * (y * z + w * x);       R[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+// Delta (dR, u) applied to pose P (reading L10): camera-centred (dR R, t + u) or world-literal
+// (dR R, dR t + u).
+__device__ __forceinline__ void apply_delta(const double dR[9], const double u[3], const double* P, int conv,
+                                            double out[12]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      out[4 * i + j] = dR[3 * i + 0] * P[j] + dR[3 * i + 1] * P[4 + j] + dR[3 * i + 2] * P[8 + j];
+    double ti = P[4 * i + 3];
+    if (conv == 1) ti = dR[3 * i + 0] * P[3] + dR[3 * i + 1] * P[7] + dR[3 * i + 2] * P[11];
+    out[4 * i + 3] = ti + u[i];
+  }
+}
+
+// Fold pose T into voxel-grid coordinates: g = (T p - o)/s - 1/2 = (R/s) p + ((t - o)/s - 1/2).
+// Returns false for non-finite or absurd poses (then every point is "outside").
+__device__ __forceinline__ bool fold_pose(const double T[12], const Geom& g, double m[12]) {
+  const double o[3] = {g.ox, g.oy, g.oz};
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) m[4 * i + j] = T[4 * i + j] / g.voxel;
+    m[4 * i + 3] = (T[4 * i + 3] - o[i]) / g.voxel - 0.5;
+  }
+#pragma unroll
+  for (int i = 0; i < 12; ++i) ok = ok && fabs(m[i]) < 1e30;
+  return ok;
+}
+
+// Template row k scaled by s = (omega deg, v cm) (reading L8): r = a*omega*pi/180, u = b*v/100.
+__device__ __forceinline__ void template_delta(const float* __restrict__ a, double omega, double v, double r[3],
+                                               double u[3]) {
+  const double ws = omega * (M_PI / 180.0), vs = v / 100.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    r[i] = (double)__ldg(a + i) * ws;
+    u[i] = (double)__ldg(a + 3 + i) * vs;
+  }
+}
+
+// ------------------------------------------------------------------ the gather-and-lerp core
+template <typename T> __device__ __forceinline__ float ldv(const T* p);
+template <> __device__ __forceinline__ float ldv<float>(const float* p) { return __ldg(p); }
+template <> __device__ __forceinline__ float ldv<__half>(const __half* p) { return __half2float(__ldg(p)); }
+
+// One particle-point evaluation (O3/O4): returns true and adds |v| to sum if the point is in band.
+template <typename T>
+__device__ __forceinline__ void eval_point(const T* __restrict__ V, const Geom& g, const double* m, double px,
+                                           double py, double pz, float& sum, unsigned& cnt) {
+  const double gx = fma(m[0], px, fma(m[1], py, fma(m[2], pz, m[3])));
+  const double gy = fma(m[4], px, fma(m[5], py, fma(m[6], pz, m[7])));
+  const double gz = fma(m[8], px, fma(m[9], py, fma(m[10], pz, m[11])));
+  const double flx = floor(gx), fly = floor(gy), flz = floor(gz);
+  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;  // saturating; finite by fold_pose
+  if ((unsigned)ix > (unsigned)(g.nx - 2) || (unsigned)iy > (unsigned)(g.ny - 2) || (unsigned)iz > (unsigned)(g.nz - 2))
+    return;
+  const float fx = (float)(gx - flx), fy = (float)(gy - fly), fz = (float)(gz - flz);
+  const uint32_t x0 = offx(ix), x1 = offx(ix + 1);
+  const uint32_t y0 = offy(iy, g.sy), y1 = offy(iy + 1, g.sy);
+  const uint32_t z0 = offz(iz, g.sz), z1 = offz(iz + 1, g.sz);
+  const float v000 = ldv(V + (x0 + y0 + z0)), v100 = ldv(V + (x1 + y0 + z0));
+  const float v010 = ldv(V + (x0 + y1 + z0)), v110 = ldv(V + (x1 + y1 + z0));
+  const float v001 = ldv(V + (x0 + y0 + z1)), v101 = ldv(V + (x1 + y0 + z1));
+  const float v011 = ldv(V + (x0 + y1 + z1)), v111 = ldv(V + (x1 + y1 + z1));
+  // in band iff all 8 corners |V| < 1 (reading L3)
+  const float amax = fmaxf(fmaxf(fmaxf(fabsf(v000), fabsf(v100)), fmaxf(fabsf(v010), fabsf(v110))),
+                           fmaxf(fmaxf(fabsf(v001), fabsf(v101)), fmaxf(fabsf(v011), fabsf(v111))));
+  if (!(amax < 1.0f)) return;
+  const float c00 = fmaf(fx, v100 - v000, v000), c10 = fmaf(fx, v110 - v010, v010);
+  const float c01 = fmaf(fx, v101 - v001, v001), c11 = fmaf(fx, v111 - v011, v011);
+  const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
+  const float val = fmaf(fz, c1 - c0, c0);
+  sum += fabsf(val);
+  cnt += 1u;
+}
+
+// Warp total of (sum, cnt) -> lane 0's fixed-point total.  All 32 lanes must call.
+__device__ __forceinline__ void warp_total(float sum, unsigned cnt, unsigned long long& S, unsigned& n) {
+  const unsigned fix = __float2uint_rn(sum * (float)kFixScale);  // sum < kPPT <= 7 -> < 2^32
+  const unsigned lo = __reduce_add_sync(0xffffffffu, fix & 0xffffu);
+  const unsigned hi = __reduce_add_sync(0xffffffffu, fix >> 16);
+  n = __reduce_add_sync(0xffffffffu, cnt);
+  S = ((unsigned long long)hi << 16) + lo;
+}
+
+struct Points { const double *x, *y, *z; int npad; };
+
+// ------------------------------------------------------------------ kernels
+struct EvalArgs {
+  const void* V;
+  Geom g;
+  Points pts;
+  int mode;                  // 0: template particles, 1: explicit poses
+  const float* pst;          // mode 0: full K x 6 template
+  int k_begin, k_count;      // particle range of this launch (absolute template rows / pose rows)
+  const TrackState* st;      // mode 0: P and s
+  int conv;
+  const double* poses;       // mode 1: M x 12
+  PartRec* acc;              // indexed by k - k_begin
+};
+
+template <typename T>
+__global__ __launch_bounds__(kThreads, 3) void k_particle_eval(EvalArgs a) {
+  __shared__ __align__(16) double sPose[kPC][12];
+  __shared__ unsigned long long sS[kPC];
+  __shared__ unsigned sN[kPC];
+  __shared__ int sOk[kPC];
+  const int c0 = blockIdx.y * kPC;
+  const int kc = min(kPC, a.k_count - c0);
+  const int tid = threadIdx.x;
+  if (tid < kc) {
+    const int k = a.k_begin + c0 + tid;
+    double T[12];
+    if (a.mode == 0) {
+      double r[3], u[3], dR[9];
+      template_delta(a.pst + 6 * (size_t)k, a.st->omega, a.st->v, r, u);
+      rodrigues(r, dR);
+      apply_delta(dR, u, a.st->P, a.conv, T);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 12; ++i) T[i] = a.poses[12 * (size_t)k + i];
+    }
+    double m[12];
+    sOk[tid] = fold_pose(T, a.g, m);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) sPose[tid][i] = m[i];
+    sS[tid] = 0ull;
+    sN[tid] = 0u;
+  }
+  // this thread's points (8x4 tiles; z == 0 marks an invalid / padding slot)
+  double px[kPPT], py[kPPT], pz[kPPT];
+#pragma unroll
+  for (int p = 0; p < kPPT; ++p) {
+    const int i = (blockIdx.x * kPPT + p) * kThreads + tid;
+    if (i < a.pts.npad) {
+      px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i];
+    } else {
+      px[p] = py[p] = pz[p] = 0.0;
+    }
+  }
+  __syncthreads();
+  const T* V = (const T*)a.V;
+  for (int j = 0; j < kc; ++j) {
+    if (!sOk[j]) continue;  // block-uniform
+    double m[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) m[i] = sPose[j][i];
+    float sum = 0.f;
+    unsigned cnt = 0u;
+#pragma unroll
+    for (int p = 0; p < kPPT; ++p)
+      if (pz[p] != 0.0) eval_point<T>(V, a.g, m, px[p], py[p], pz[p], sum, cnt);
+    unsigned long long S;
+    unsigned n;
+    warp_total(sum, cnt, S, n);
+    if ((tid & 31) == 0 && n) {
+      atomicAdd(&sS[j], S);
+      atomicAdd(&sN[j], n);
+    }
+  }
+  __syncthreads();
+  if (tid < kc && sN[tid]) {
+    PartRec* r = a.acc + (c0 + tid);
+    atomicAdd(&r->S, sS[tid]);
+    atomicAdd(&r->n, sN[tid]);
+  }
+}
+
+// E from a fixed-point record (O4; reading L6): S/n if n > 0 and n >= rho N, else 1.
+__device__ __forceinline__ double fitness_of(unsigned long long S, unsigned n, double rho, int N) {
+  if (n > 0u && (double)n >= rho * (double)N) return ((double)S * kFixInv) / (double)n;
+  return 1.0;
+}
+
+struct TrackArgs {
+  TrackState* st;
+  const double* T_init;
+  double omega0, v0, beta, rho;
+  int conv;
+  PartRec* acc_local;
+  int kloc;
+};
+
+__global__ void k_track_init(TrackArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    TrackState* s = a.st;
+    for (int j = 0; j < 12; ++j) s->P[j] = a.T_init[j];
+    s->omega = a.omega0; s->v = a.v0;
+    s->Ec = 1.0; s->Ebase = 1.0;
+    s->Sc_acc = 0ull; s->nc_acc = 0u; s->nc = 0u;
+    s->nA = 0; s->iter = 0; s->Nvalid = 0;
+    s->ticket_upd = 0u; s->ticket_ctr = 0u;
+  }
+  for (int k = i; k < a.kloc; k += gridDim.x * blockDim.x) {
+    a.acc_local[k].S = 0ull;
+    a.acc_local[k].n = 0u;
+    a.acc_local[k].pad = 0u;
+  }
+}
+
+// O1/O2: points of the strided pixel grid (sigma c, sigma r), r < nr, c < nc, in 8x4 tiles.
+struct BPArgs {
+  const uint16_t* depth;
+  double fx, fy, cx, cy, unit, max_depth;
+  int W, H, stride, nr, nc, ntx, npad;
+  double *x, *y, *z;
+  int* Nvalid;
+};
+
+__global__ void k_backproject(BPArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.npad) return;
+  const int t = i >> 5, l = i & 31;
+  const int r = (t / a.ntx) * 4 + (l >> 3), c = (t % a.ntx) * 8 + (l & 7);
+  double X = 0.0, Y = 0.0, Z = 0.0;
+  bool valid = false;
+  if (r < a.nr && c < a.nc) {
+    const int u = c * a.stride, v = r * a.stride;
+    const uint16_t raw = a.depth[(size_t)v * a.W + u];
+    const double d = __dmul_rn((double)raw, a.unit);
+    if (raw != 0 && d < a.max_depth) {
+      valid = true;
+      X = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, a.cx), d), a.fx);
+      Y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, a.cy), d), a.fy);
+      Z = d;
+    }
+  }
+  a.x[i] = X; a.y[i] = Y; a.z[i] = Z;
+  const unsigned b = __ballot_sync(0xffffffffu, valid);
+  if (l == 0 && b) atomicAdd(a.Nvalid, __popc(b));
+}
+
+// a5 + a8: E(P) of the current pose; the last CTA closes the iteration (s-law, trace).
+struct CentreArgs {
+  const void* V;
+  Geom g;
+  Points pts;
+  TrackState* st;
+  int initial;          // 1: baseline E(T_init) before iteration 1 (no s-update, no trace)
+  double beta, rho;
+  double* trace;        // NULL or iters x PFT_TRACE_DOUBLES
+  double* T_out;        // written by the last CTA of every call
+};
+
+template <typename T>
+__global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
+  __shared__ double sm[12];
+  __shared__ int sOk;
+  __shared__ bool sLast;
+  TrackState* st = a.st;
+  const bool do_eval = a.initial || st->nA > 0;
+  const int tid = threadIdx.x;
+  if (do_eval) {
+    if (tid == 0) {
+      double P[12], m[12];
+      for (int i = 0; i < 12; ++i) P[i] = st->P[i];
+      sOk = fold_pose(P, a.g, m);
+      for (int i = 0; i < 12; ++i) sm[i] = m[i];
+    }
+    __syncthreads();
+    float sum = 0.f;
+    unsigned cnt = 0u;
+    if (sOk) {
+      double m[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) m[i] = sm[i];
+#pragma unroll
+      for (int p = 0; p < kPPT; ++p) {
+        const int i = (blockIdx.x * kPPT + p) * kThreads + tid;
+        if (i < a.pts.npad) {
+          const double z = a.pts.z[i];
+          if (z != 0.0) eval_point<T>((const T*)a.V, a.g, m, a.pts.x[i], a.pts.y[i], z, sum, cnt);
+        }
+      }
+    }
+    unsigned long long S;
+    unsigned n;
+    warp_total(sum, cnt, S, n);
+    if ((tid & 31) == 0 && n) {
+      atomicAdd(&st->Sc_acc, S);
+      atomicAdd(&st->nc_acc, n);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sLast = atomicAdd(&st->ticket_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!sLast || tid != 0) return;
+  __threadfence();
+  volatile TrackState* vs = st;
+  double Ec = vs->Ec;
+  unsigned nc = vs->nc;
+  if (do_eval) {
+    const unsigned long long S = vs->Sc_acc;
+    nc = vs->nc_acc;
+    Ec = fitness_of(S, nc, a.rho, vs->Nvalid);
+  }
+  st->Sc_acc = 0ull;
+  st->nc_acc = 0u;
+  st->ticket_ctr = 0u;
+  st->Ec = Ec;
+  st->nc = nc;
+  if (!a.initial) {
+    // s^(i+1) = beta s^(i) + (1 - beta) E(P^(i)) s^(i), as (beta + (1-beta)E) s
+    const double om = vs->omega, v = vs->v;
+    const double factor = __dadd_rn(a.beta, __dmul_rn(__dsub_rn(1.0, a.beta), Ec));
+    const double om1 = __dmul_rn(factor, om), v1 = __dmul_rn(factor, v);
+    st->omega = om1;
+    st->v = v1;
+    const int it = vs->iter;
+    if (a.trace) {
+      double* r = a.trace + (size_t)it * PFT_TRACE_DOUBLES;
+      const int nA = vs->nA;
+      const int N = vs->Nvalid;
+      r[0] = vs->Ebase; r[1] = (double)nA; r[2] = om; r[3] = v;
+      for (int i = 0; i < 12; ++i) r[4 + i] = vs->P[i];
+      r[16] = Ec; r[17] = om1; r[18] = v1;
+      r[19] = (double)((nA == 0 ? 1 : 0) | (vs->Ebase == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0));
+      r[20] = (double)nc; r[21] = (double)N; r[22] = 0.0; r[23] = 0.0;
+    }
+    st->iter = it + 1;
+  }
+  if (a.T_out)
+    for (int i = 0; i < 12; ++i) a.T_out[i] = vs->P[i];
+}
+
+// a7: E_k, advantage set A = {k : E_k < E_c}, mean delta over A,
+// P <- (R(q), u) P.  nblk CTAs of 256 threads, one particle per thread; each CTA
+// reduces its members in a fixed tree, the last CTA combines the CTA partials in a fixed tree.
+struct UpdArgs {
+  TrackState* st;
+  const PartRec* full;       // K records (all ranks)
+  PartRec* local;            // this rank's records, zeroed for the next iteration
+  int K, k_begin, kloc;      // local covers global [k_begin, k_begin + kloc)
+  const float* pst;
+  int conv;
+  double rho;
+  double* E_out;
+  int* n_out;
+  double* partials;          // nblk x 8
+};
+
+__global__ __launch_bounds__(256) void k_update(UpdArgs a) {
+  __shared__ double red[8][256];
+  __shared__ bool sLast;
+  TrackState* st = a.st;
+  const int tid = threadIdx.x;
+  const int k = blockIdx.x * 256 + tid;
+  const double Ec = st->Ec;
+  const int N = st->Nvalid;
+  double q[4] = {0.0, 0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, member = 0.0;
+  if (k < a.K) {
+    const PartRec rec = a.full[k];
+    const double E = fitness_of(rec.S, rec.n, a.rho, N);
+    a.E_out[k] = E;
+    a.n_out[k] = (int)rec.n;
+    if (E < Ec) {
+      double r[3];
+      template_delta(a.pst + 6 * (size_t)k, st->omega, st->v, r, u);
+      rotvec_quat(r, q);
+      member = 1.0;
+    }
+    const int j = k - a.k_begin;
+    if (j >= 0 && j < a.kloc) {
+      a.local[j].S = 0ull;
+      a.local[j].n = 0u;
+    }
+  }
+  red[0][tid] = q[0]; red[1][tid] = q[1]; red[2][tid] = q[2]; red[3][tid] = q[3];
+  red[4][tid] = u[0]; red[5][tid] = u[1]; red[6][tid] = u[2]; red[7][tid] = member;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
+    __syncthreads();
+  }
+  if (tid < 8) a.partials[blockIdx.x * 8 + tid] = red[tid][0];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sLast = atomicAdd(&st->ticket_upd, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!sLast) return;
+  __threadfence();
+  // fixed-order combine of the CTA partials
+#pragma unroll
+  for (int c = 0; c < 8; ++c) red[c][tid] = 0.0;
+  for (int b = tid; b < (int)gridDim.x; b += 256)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) red[c][tid] += __ldcg(a.partials + b * 8 + c);
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int nA = (int)red[7][0];
+    st->nA = nA;
+    st->Ebase = Ec;
+    st->ticket_upd = 0u;
+    if (nA > 0) {
+      const double Q[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
+      const double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
+      const double qb[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
+      const double ub[3] = {red[4][0] / nA, red[5][0] / nA, red[6][0] / nA};
+      double Rb[9], P[12], Pn[12];
+      quat_to_R(qb, Rb);
+      for (int i = 0; i < 12; ++i) P[i] = st->P[i];
+      apply_delta(Rb, ub, P, a.conv, Pn);
+      for (int i = 0; i < 12; ++i) st->P[i] = Pn[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles, int32_t stride,
+                        int nranks, TrackLayout* L) {
+  (void)vol;
+  if (nparticles < 1) return fail(PFT_ERR_INVALID_ARG, "number of particles/poses must be >= 1");
+  if (stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
+  pft_status s = check_intrinsics(K);
+  if (s != PFT_OK) return s;
+  L->nr = (K->height + stride - 1) / stride;
+  L->nc = (K->width + stride - 1) / stride;
+  L->ntx = (L->nc + 7) / 8;
+  L->nty = (L->nr + 3) / 4;
+  L->npad = L->ntx * L->nty * 32;
+  L->kloc = (nparticles + nranks - 1) / nranks;
+  L->kfull = L->kloc * nranks;
+  L->nblk_upd = (nparticles + 255) / 256;
+  size_t off = 0;
+  L->state_off = off; off = align_up(off + sizeof(TrackState), 256);
+  L->pts_off = off; off = align_up(off + 3 * sizeof(double) * (size_t)L->npad, 256);
+  L->acc_local_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kloc, 256);
+  if (nranks > 1) { L->acc_full_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kfull, 256); }
+  else L->acc_full_off = L->acc_local_off;
+  L->part_off = off; off = align_up(off + 8 * sizeof(double) * (size_t)L->nblk_upd, 256);
+  L->total = off;
+  return PFT_OK;
+}
+
+pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st);
+
+struct Launch {
+  pft_volume* vol;
+  TrackLayout L;
+  char* ws;
+  cudaStream_t st;
+  TrackState* state() const { return (TrackState*)(ws + L.state_off); }
+  Points pts() const {
+    double* p = (double*)(ws + L.pts_off);
+    return Points{p, p + L.npad, p + 2 * (size_t)L.npad, L.npad};
+  }
+};
+
+static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_intrinsics* K, int stride,
+                            const double* T_init, double omega0, double v0, int conv) {
+  TrackArgs ta{c.state(), T_init, omega0, v0, 0.0, 0.0, conv, (PartRec*)(c.ws + c.L.acc_local_off), c.L.kloc};
+  int gi = (c.L.kloc + 255) / 256;
+  PFT_LAUNCH(PFT_PROF_PREP, c.st, k_track_init<<<gi < 148 ? gi : 148, 256, 0, c.st>>>(ta));
+  Points P = c.pts();
+  BPArgs b{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height, stride,
+           c.L.nr, c.L.nc, c.L.ntx, c.L.npad, (double*)P.x, (double*)P.y, (double*)P.z, &c.state()->Nvalid};
+  PFT_LAUNCH(PFT_PROF_PREP, c.st, k_backproject<<<(c.L.npad + 255) / 256, 256, 0, c.st>>>(b));
+}
+
+template <typename T>
+static void launch_centre(const Launch& c, int initial, double beta, double rho, double* trace, double* T_out) {
+  CentreArgs ca{c.vol->base + c.vol->L.v_off, c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
+  int grid = (c.L.npad + kPointsPerCTA - 1) / kPointsPerCTA;
+  PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
+}
+
+template <typename T>
+static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin, int k_count, int conv,
+                        const double* poses, PartRec* acc) {
+  if (k_count <= 0) return;
+  EvalArgs ea{c.vol->base + c.vol->L.v_off, c.vol->g, c.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
+  dim3 grid((c.L.npad + kPointsPerCTA - 1) / kPointsPerCTA, (k_count + kPC - 1) / kPC);
+  PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T><<<grid, kThreads, 0, c.st>>>(ea));
+}
+
+template <typename T>
+static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
+                            const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
+                            int32_t* n_out, double* trace) {
+  const int G = c.vol->nranks, r = c.vol->rank;
+  const int kloc = c.L.kloc;
+  const int k_begin = r * kloc;
+  const int k_count = max(0, min(Kp, k_begin + kloc) - k_begin);
+  PartRec* local = (PartRec*)(c.ws + c.L.acc_local_off);
+  PartRec* full = (PartRec*)(c.ws + c.L.acc_full_off);
+  launch_prologue(c, depth, K, prm->stride, T_init, prm->omega0_deg, prm->v0_cm, prm->delta_conv);
+  launch_centre<T>(c, 1, prm->beta, prm->min_inband_frac, nullptr, nullptr);
+  for (int it = 0; it < prm->iters; ++it) {
+    launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local);
+    if (G > 1) {
+      pft_status s = comm_allgather(c.vol, local, full, sizeof(PartRec) * (size_t)kloc, c.st);
+      if (s != PFT_OK) return s;
+    }
+    UpdArgs ua{c.state(), full, local, Kp, k_begin, kloc, pst, prm->delta_conv, prm->min_inband_frac, E, n_out,
+               (double*)(c.ws + c.L.part_off)};
+    PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_update<<<c.L.nblk_upd, 256, 0, c.st>>>(ua));
+    launch_centre<T>(c, 0, prm->beta, prm->min_inband_frac, trace, it == prm->iters - 1 ? T_out : nullptr);
+  }
+  return cuda_check("track");
+}
+
+// per-pose results of an eval_poses call
+__global__ void k_finish_poses(const PartRec* acc, int M, const TrackState* st, double rho, double* E, int* n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  const PartRec r = acc[k];
+  E[k] = fitness_of(r.S, r.n, rho, st->Nvalid);
+  n[k] = (int)r.n;
+}
+
+static pft_status check_params(const pft_track_params* p) {
+  if (!p) return fail(PFT_ERR_INVALID_ARG, "params is NULL");
+  if (!(p->beta >= 0.0 && p->beta < 1.0)) return fail(PFT_ERR_INVALID_ARG, "beta must be in [0,1) (SPEC.md:313)");
+  if (p->iters < 1) return fail(PFT_ERR_INVALID_ARG, "iters must be >= 1");
+  if (!(p->omega0_deg >= 0.0 && p->omega0_deg <= 100.0)) return fail(PFT_ERR_INVALID_ARG, "omega0_deg must be in [0,100]");
+  if (!(p->v0_cm >= 0.0 && p->v0_cm < 1e6)) return fail(PFT_ERR_INVALID_ARG, "v0_cm must be in [0,1e6)");
+  if (p->stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
+  if (!(p->min_inband_frac >= 0.0 && p->min_inband_frac <= 1.0)) return fail(PFT_ERR_INVALID_ARG, "min_inband_frac must be in [0,1]");
+  if (p->delta_conv != PFT_DELTA_CAMERA_CENTRED && p->delta_conv != PFT_DELTA_WORLD_LITERAL)
+    return fail(PFT_ERR_INVALID_ARG, "bad delta_conv");
+  if (p->update_rule != PFT_UPDATE_MEAN) return fail(PFT_ERR_UNSUPPORTED, "only PFT_UPDATE_MEAN is implemented");
+  return PFT_OK;
+}
+
+}  // namespace pft
+
+using namespace pft;
+
+extern "C" {
+
+pft_status pft_track_workspace_bytes(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
+                                     const pft_track_params* prm, size_t* bytes_out) {
+  if (!vol || !bytes_out || !prm) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  TrackLayout L;
+  pft_status s = track_layout(vol, K, nparticles, prm->stride, vol->nranks, &L);
+  if (s != PFT_OK) return s;
+  *bytes_out = L.total;
+  return PFT_OK;
+}
+
+pft_status pft_track(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K, const double* dev_T_init,
+                     const float* dev_pst, int32_t nparticles, const pft_track_params* prm, void* dev_ws,
+                     size_t ws_bytes, double* dev_T_out, double* dev_E, int32_t* dev_inband, double* dev_trace,
+                     void* stream) {
+  if (!vol || !dev_depth || !dev_T_init || !dev_pst || !dev_ws || !dev_T_out || !dev_E || !dev_inband)
+    return fail(PFT_ERR_INVALID_ARG, "NULL required argument");
+  pft_status s = check_params(prm);
+  if (s != PFT_OK) return s;
+  Launch c;
+  c.vol = vol;
+  c.ws = (char*)dev_ws;
+  c.st = (cudaStream_t)stream;
+  s = track_layout(vol, K, nparticles, prm->stride, vol->nranks, &c.L);
+  if (s != PFT_OK) return s;
+  if (ws_bytes < c.L.total) return fail(PFT_ERR_BUFFER_TOO_SMALL, "workspace %zu B < required %zu B", ws_bytes, c.L.total);
+  if (((uintptr_t)dev_ws) % 256) return fail(PFT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (vol->esize == 4)
+    return track_run<float>(c, dev_depth, K, dev_T_init, dev_pst, nparticles, prm, dev_T_out, dev_E, dev_inband, dev_trace);
+  return track_run<__half>(c, dev_depth, K, dev_T_init, dev_pst, nparticles, prm, dev_T_out, dev_E, dev_inband, dev_trace);
+}
+
+pft_status pft_eval_poses(const pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K,
+                          const pft_track_params* prm, const double* dev_poses, int32_t M, void* dev_ws,
+                          size_t ws_bytes, double* dev_E, int32_t* dev_inband, void* stream) {
+  if (!vol || !dev_depth || !prm || !dev_poses || !dev_ws || !dev_E || !dev_inband)
+    return fail(PFT_ERR_INVALID_ARG, "NULL required argument");
+  if (prm->stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
+  if (!(prm->min_inband_frac >= 0.0 && prm->min_inband_frac <= 1.0)) return fail(PFT_ERR_INVALID_ARG, "min_inband_frac must be in [0,1]");
+  Launch c;
+  c.vol = (pft_volume*)vol;
+  c.ws = (char*)dev_ws;
+  c.st = (cudaStream_t)stream;
+  // eval_poses is rank-local: lay the workspace out for one rank
+  pft_status s = track_layout(vol, K, M, prm->stride, 1, &c.L);
+  if (s != PFT_OK) return s;
+  if (ws_bytes < c.L.total) return fail(PFT_ERR_BUFFER_TOO_SMALL, "workspace %zu B < required %zu B", ws_bytes, c.L.total);
+  if (((uintptr_t)dev_ws) % 256) return fail(PFT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  // (the state's pose is initialised from pose 0; eval_poses never reads it)
+  launch_prologue(c, dev_depth, K, prm->stride, dev_poses, 0.0, 0.0, 0);
+  PartRec* acc = (PartRec*)(c.ws + c.L.acc_local_off);
+  if (vol->esize == 4) launch_eval<float>(c, 1, nullptr, 0, M, 0, dev_poses, acc);
+  else launch_eval<__half>(c, 1, nullptr, 0, M, 0, dev_poses, acc);
+  PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_finish_poses<<<(M + 255) / 256, 256, 0, c.st>>>(acc, M, c.state(), prm->min_inband_frac, dev_E, dev_inband));
+  return cuda_check("eval_poses");
+}
+
+pft_status pft_track_info(const void* dev_ws, int32_t* npoints_out, void* stream) {
+  if (!dev_ws || !npoints_out) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int n = 0;
+  const TrackState* s = (const TrackState*)dev_ws;  // state is at offset 0 of every layout
+  if (cudaMemcpyAsync(&n, &s->Nvalid, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return cuda_check("track_info");
+  *npoints_out = n;
+  return PFT_OK;
+}
+
+}  // extern "C"

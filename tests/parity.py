@@ -1,0 +1,55 @@
+"""Parity helpers: GPU (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star): in-band counts bit-exact; E within
+1e-5 relative (1e-9 absolute floor); TSDF voxels within 1e-5 absolute (here: bit-exact, since
+the fusion arithmetic is evaluated in the same fp64 operation order on both sides); poses
+within 1e-4 m and 1e-4 rad.  A count mismatch is accepted only as a "tie": the oracle's cell
+decision margin (distance of a grid coordinate to an integer) below 1e-9 voxel units.
+"""
+import numpy as np
+
+import oracle
+
+E_REL, E_ABS = 1e-5, 1e-9
+POSE_M, POSE_RAD = 1e-4, 1e-4
+TIE_MARGIN = 1e-9
+
+
+def close_E(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.abs(a - b) <= np.maximum(E_REL * np.abs(b), E_ABS)
+
+
+def assert_eval_parity(E_gpu, n_gpu, ora, what=""):
+    """ora: dict(E, n, margin) from OracleVolume.eval_poses."""
+    n_gpu = np.asarray(n_gpu)
+    bad_n = n_gpu != ora["n"]
+    ties = bad_n & (ora["margin"] < TIE_MARGIN)
+    real = bad_n & ~ties
+    assert not real.any(), f"{what}: in-band count mismatch at {np.nonzero(real)[0][:10]} " \
+                           f"gpu={n_gpu[real][:5]} oracle={ora['n'][real][:5]} margin={ora['margin'][real][:5]}"
+    ok = close_E(E_gpu, ora["E"]) | bad_n
+    assert ok.all(), f"{what}: E mismatch at {np.nonzero(~ok)[0][:10]}: gpu={np.asarray(E_gpu)[~ok][:5]} " \
+                     f"oracle={ora['E'][~ok][:5]}"
+    return int(ties.sum())
+
+
+def assert_pose_close(Ta, Tb, what=""):
+    Ta, Tb = np.asarray(Ta).reshape(3, 4), np.asarray(Tb).reshape(3, 4)
+    dt = np.abs(Ta[:, 3] - Tb[:, 3]).max()
+    dr = oracle.rotation_error_rad(Ta, Tb)
+    assert dt <= POSE_M and dr <= POSE_RAD, f"{what}: pose differs by {dt:.3e} m / {dr:.3e} rad"
+
+
+def assert_trace_parity(tr_gpu, tr_ora, what=""):
+    """Per-iteration: |A| exact, E_base / E(P) 1e-5 rel, s 1e-6 rel, P 1e-4, flags exact."""
+    tr_gpu = np.asarray(tr_gpu)
+    for i in range(tr_ora.shape[0]):
+        g, o = tr_gpu[i], tr_ora[i]
+        w = f"{what} iter {i + 1}"
+        assert g[1] == o[1], f"{w}: |A| gpu={g[1]} oracle={o[1]}"
+        assert close_E(g[0], o[0]) and close_E(g[16], o[16]), f"{w}: E gpu={g[[0, 16]]} oracle={o[[0, 16]]}"
+        for j in (2, 3, 17, 18):
+            assert abs(g[j] - o[j]) <= 1e-6 * abs(o[j]) + 1e-12, f"{w}: s[{j}] gpu={g[j]} oracle={o[j]}"
+        assert_pose_close(g[4:16], o[4:16], w)
+        assert g[19] == o[19], f"{w}: flags gpu={g[19]} oracle={o[19]}"

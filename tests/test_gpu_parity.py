@@ -1,0 +1,306 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by element, on
+seeded synthetic inputs (BASELINE.json configs) and the hand-derived golden fixtures."""
+import numpy as np
+import pytest
+
+import oracle
+from synth.configs import (KINECT_VGA, TrackParams, VolumeDesc, config_single, config_tiny, init_noise, make_pst,
+                           with_desc)
+from synth.rng import Stream
+from synth.scene import Intrinsics, analytic_fill, box_room, perturb, render_depth
+from tests.fixtures import f_track_inputs, golden
+from tests.parity import assert_eval_parity, assert_pose_close, assert_trace_parity, close_E
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def pft():
+    import paper_2509_24236_b200 as m
+    m.lib()
+    return m
+
+
+def dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def T(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    return (t if dtype is None else t.to(dtype)).to(dev())
+
+
+def gpu_volume(pft, desc, V=None, W=None):
+    vol = pft.Volume(desc, dev())
+    if V is None:
+        vol.reset()
+    else:
+        vol.upload(V, W)
+    return vol
+
+
+def run_track(pft, vol, depth, intr, T_init, pst, params):
+    r = vol.track(T(depth), intr, T(T_init), T(pst), params)
+    torch.cuda.synchronize()
+    return {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in r.items() if k != "ws"}
+
+
+def storage_bits(x):
+    x = np.asarray(x)
+    return x.view(np.uint32) if x.dtype.itemsize == 4 else x.view(np.uint16)
+
+
+# ------------------------------------------------------------------ golden fixtures
+def test_f_track_golden(pft):
+    f = f_track_inputs()
+    vol = gpu_volume(pft, f["desc"], f["V"], f["W"])
+    r = run_track(pft, vol, f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
+    a = float(np.float32(1.0 / 6.0))
+    tr = r["trace"]
+    # iteration 1: E_base = 0.5a, |A| = 1, P = GT, E_c = 0, s -> (1, 1)
+    assert abs(tr[0, 0] - 0.5 * a) < 1e-8 and tr[0, 1] == 1 and tr[0, 16] == 0.0
+    assert tr[0, 17] == pytest.approx(1.0, abs=1e-12) and tr[0, 18] == pytest.approx(1.0, abs=1e-12)
+    # iteration 2: |A| = 0, s -> (0.1, 0.1)
+    assert tr[1, 1] == 0 and tr[1, 17] == pytest.approx(0.1, abs=1e-12)
+    np.testing.assert_allclose(r["T"], f["T_gt"], atol=1e-12)
+    np.testing.assert_array_equal(r["n"], [4, 4])
+    np.testing.assert_allclose(r["E"], [0.0, 0.05 * a], atol=1e-8)
+    # and against the oracle
+    o = oracle.OracleVolume(f["desc"], f["V"], f["W"]).track(f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
+    assert_trace_parity(tr, o["trace"], "F-track")
+    vol.close()
+
+
+def test_f_integrate_golden(pft):
+    f = f_track_inputs()
+    g = golden("f_integrate.json")
+    for full in (False, True):
+        vol = gpu_volume(pft, f["desc"])
+        vol.integrate(T(f["depth"]), f["intr"], T(f["T_gt"]), full_sweep=full)
+        V, W = [x.cpu().numpy().reshape(16, 16, 16) for x in vol.download()]
+        i, j = g["column_ij"]
+        exp_V = [float(eval(s)) for s in g["V"]]
+        np.testing.assert_allclose(V[:, j, i], exp_V, atol=1e-7)
+        np.testing.assert_array_equal(W[:, j, i], g["W"])
+        assert int((W > 0).sum()) == g["updated_voxels"]
+        ov = oracle.OracleVolume(f["desc"])
+        ov.integrate(f["depth"], f["intr"], f["T_gt"])
+        assert np.array_equal(storage_bits(V.ravel()), storage_bits(ov.V))
+        assert np.array_equal(storage_bits(W.ravel()), storage_bits(ov.W))
+        vol.close()
+
+
+# ------------------------------------------------------------------ eval_poses (K2 in isolation)
+def _pose_cloud(T_gt, seed, M, deg, cm):
+    st = Stream(seed, 77)
+    ab = st.symmetric(6 * M).reshape(M, 6)
+    return np.stack([perturb(T_gt, a[:3], a[3:], deg, cm) for a in ab])
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_eval_poses_tiny(pft, storage):
+    c = config_tiny(seed=1)
+    desc = with_desc(c, storage=storage)["desc"]
+    V, W = c["V"], c["W"]
+    if storage == "f16":
+        V, W = V.astype(np.float16), W.astype(np.float16)
+    poses = np.concatenate([c["T_gt"][None], _pose_cloud(c["T_gt"], 1, 300, 3.0, 3.0),
+                            _pose_cloud(c["T_gt"], 2, 60, 40.0, 60.0)])
+    vol = gpu_volume(pft, desc, V, W)
+    params = TrackParams(stride=1)
+    r = vol.eval_poses(T(c["depth"]), c["intr"], T(poses), params)
+    torch.cuda.synchronize()
+    ov = oracle.OracleVolume(desc, V.view(np.uint16) if storage == "f16" else V,
+                             W.view(np.uint16) if storage == "f16" else W)
+    o = ov.eval_poses(c["depth"], c["intr"], poses, stride=1)
+    assert vol.npoints(r["ws"]) == o["N"] == 4800
+    assert_eval_parity(r["E"].cpu().numpy(), r["n"].cpu().numpy(), o, f"tiny {storage}")
+    assert (o["n"] > 0).sum() > 200   # the cloud really exercises the band
+    vol.close()
+
+
+def test_eval_poses_single_room(pft):
+    """Config S geometry (256^3 @ 1 cm, 640x480 -> 160x120 points); poses span in-band,
+    partially-outside and fully-outside cases, several 8x4 tiles and the ragged last CTA."""
+    c = config_single(seed=1)
+    poses = np.concatenate([c["T_gt"][None], _pose_cloud(c["T_gt"], 3, 96, 8.0, 8.0),
+                            _pose_cloud(c["T_gt"], 4, 31, 90.0, 150.0)])
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    r = vol.eval_poses(T(c["depth"]), c["intr"], T(poses), c["params"])
+    torch.cuda.synchronize()
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).eval_poses(c["depth"], c["intr"], poses, stride=4)
+    assert o["N"] == vol.npoints(r["ws"])
+    assert_eval_parity(r["E"].cpu().numpy(), r["n"].cpu().numpy(), o, "single")
+    vol.close()
+
+
+@pytest.mark.parametrize("stride", [1, 3, 5])
+def test_eval_poses_strides_and_ragged_image(pft, stride):
+    """Ragged strided grids (ceil(H/s) x ceil(W/s) not multiples of the 8x4 tile) and a
+    depth map with invalid pixels (0 and >= max_depth)."""
+    c = config_tiny(seed=2)
+    depth = c["depth"].copy()
+    st = Stream(9, 9)
+    holes = st.uniform(depth.size).reshape(depth.shape)
+    depth[holes < 0.1] = 0
+    depth[(holes >= 0.1) & (holes < 0.15)] = 9000  # 9 m >= max_depth 8 m: invalid
+    depth = depth[:57, :75].copy()
+    intr = Intrinsics(131.25, 131.25, 37.0, 28.0, 75, 57)
+    poses = np.concatenate([c["T_gt"][None], _pose_cloud(c["T_gt"], 5, 40, 3.0, 3.0)])
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    r = vol.eval_poses(T(depth), intr, T(poses), TrackParams(stride=stride, min_inband_frac=0.3))
+    torch.cuda.synchronize()
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).eval_poses(depth, intr, poses, stride=stride, rho=0.3)
+    assert o["N"] == vol.npoints(r["ws"])
+    assert_eval_parity(r["E"].cpu().numpy(), r["n"].cpu().numpy(), o, f"stride {stride}")
+    vol.close()
+
+
+# ------------------------------------------------------------------ track (whole RO loop)
+@pytest.mark.parametrize("conv", [0, 1])
+def test_track_tiny(pft, conv):
+    c = config_tiny(seed=1)
+    params = TrackParams(iters=3, stride=1, delta_conv=conv)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], params)
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], c["pst"], params)
+    assert_trace_parity(r["trace"], o["trace"], f"tiny conv={conv}")
+    np.testing.assert_array_equal(r["n"], o["n"])
+    assert close_E(r["E"], o["E"]).all()
+    assert_pose_close(r["T"], o["T"], "tiny final")
+    assert np.all(r["trace"][:, 21] == 4800)
+    vol.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_track_single(pft, seed):
+    """Config S in full: 256^3 @1 cm, 1024 particles, 10 iterations, +-8 deg/cm init."""
+    c = config_single(seed=seed)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
+    assert_trace_parity(r["trace"], o["trace"], f"single seed {seed}")
+    np.testing.assert_array_equal(r["n"], o["n"])
+    assert close_E(r["E"], o["E"]).all()
+    assert_pose_close(r["T"], o["T"], "single final")
+    vol.close()
+
+
+def test_track_ragged_K_and_prefix_stable_and_deterministic(pft):
+    c = config_tiny(seed=3)
+    pst = make_pst(3, 37)  # not a multiple of the 32-particle CTA chunk
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    p3 = TrackParams(iters=3, stride=1)
+    p2 = TrackParams(iters=2, stride=1)
+    a = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, p3)
+    b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, p3)
+    d = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, p2)
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(a[k], b[k]), f"non-deterministic {k}"
+    assert np.array_equal(a["trace"][:2], d["trace"]), "not prefix-stable"
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], pst, p3)
+    assert_trace_parity(a["trace"], o["trace"], "K=37")
+    np.testing.assert_array_equal(a["n"], o["n"])
+    vol.close()
+
+
+def test_track_single_particle_and_empty_cloud(pft):
+    c = config_tiny(seed=1)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    p = TrackParams(iters=2, stride=1)
+    one = make_pst(5, 1)
+    a = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], one, p)
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], one, p)
+    assert_trace_parity(a["trace"], o["trace"], "K=1")
+    # empty cloud: T_out = T_init, E = 1, n = 0, trace flag bit 2
+    z = np.zeros_like(c["depth"])
+    e = run_track(pft, vol, z, c["intr"], c["T_init"], c["pst"], p)
+    np.testing.assert_array_equal(e["T"], c["T_init"])
+    assert np.all(e["E"] == 1.0) and np.all(e["n"] == 0)
+    assert all(int(f) & 4 for f in e["trace"][:, 19])
+    vol.close()
+
+
+# ------------------------------------------------------------------ integration
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_integrate_room_bit_exact(pft, storage):
+    """Three frames of the room fused into a reset 128^3 volume @2 cm (GPU culled path and
+    full sweep vs oracle): stored values and weights bit-identical."""
+    scene = box_room(seed=4)
+    desc = VolumeDesc(128, 128, 128, 0.02, (-1.28, -1.28, -1.28), 0.06, storage=storage)
+    intr = Intrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    from synth.configs import room_gt_pose
+    T_gt = room_gt_pose(scene, 4)
+    vol = gpu_volume(pft, desc)
+    vol_full = gpu_volume(pft, desc)
+    ov = oracle.OracleVolume(desc)
+    for f in range(3):
+        Tf = perturb(T_gt, [0.0, 0.0, 0.1 * f], [0.05 * f, 0.0, 0.0], 10.0, 10.0)
+        depth = render_depth(scene, intr, Tf, Stream(4, 4_000_000 + f))
+        vol.integrate(T(depth), intr, T(Tf))
+        vol_full.integrate(T(depth), intr, T(Tf), full_sweep=True)
+        ov.integrate(depth, intr, Tf)
+    V, W = [x.cpu().numpy() for x in vol.download()]
+    Vf, Wf = [x.cpu().numpy() for x in vol_full.download()]
+    assert np.array_equal(storage_bits(V), storage_bits(Vf)) and np.array_equal(storage_bits(W), storage_bits(Wf))
+    assert np.array_equal(storage_bits(V), storage_bits(ov.V)), \
+        f"{int((storage_bits(V) != storage_bits(ov.V)).sum())} voxel values differ"
+    assert np.array_equal(storage_bits(W), storage_bits(ov.W))
+    assert vol.checksum() == vol_full.checksum()
+    assert (ov.weights_f64() > 0).sum() > 10000
+    vol.close()
+    vol_full.close()
+
+
+def test_upload_download_roundtrip_and_checksum(pft):
+    desc = VolumeDesc(37, 18, 23, 0.05, (0.0, 0.0, 0.0), 0.2)   # ragged bricks on every axis
+    st = Stream(11, 11)
+    V = st.symmetric(37 * 18 * 23).astype(np.float32)
+    W = np.floor(st.uniform(37 * 18 * 23) * 5).astype(np.float32)
+    vol = gpu_volume(pft, desc, V, W)
+    V2, W2 = [x.cpu().numpy() for x in vol.download()]
+    assert np.array_equal(V, V2) and np.array_equal(W, W2)
+    h1 = vol.checksum()
+    vol2 = gpu_volume(pft, desc, V, W)
+    assert vol2.checksum() == h1
+    W[5] += 1
+    vol2.upload(V, W)
+    assert vol2.checksum() != h1
+    vol.close()
+    vol2.close()
+
+
+def test_sequence_track_then_integrate(pft):
+    """Config-Q-like loop at reduced size: frame 0 integrated at GT, then 3 frames of
+    track (K=256, 5 iterations) + integrate at the tracked pose, GPU and oracle in lock step;
+    voxels bit-exact after every frame, poses within 1e-4."""
+    from synth.configs import shaky_trajectory
+    from synth.scene import compose, inverse
+    scene = box_room(seed=6)
+    desc = VolumeDesc(160, 160, 160, 0.02, (-1.6, -1.6, -1.6), 0.06)
+    intr = Intrinsics(262.5, 262.5, 159.5, 119.5, 320, 240)
+    gt = shaky_trajectory(scene, 40, seed=6)
+    pst = make_pst(6, 256)
+    params = TrackParams(iters=5, stride=4)
+    vol = gpu_volume(pft, desc)
+    ov = oracle.OracleVolume(desc)
+    d0 = render_depth(scene, intr, gt[0], Stream(6, 4_000_000))
+    vol.integrate(T(d0), intr, T(gt[0]))
+    ov.integrate(d0, intr, gt[0])
+    P_prev = gt[0]
+    for t in range(1, 4):
+        depth = render_depth(scene, intr, gt[t], Stream(6, 4_000_000 + t))
+        rel = init_noise(6, t, compose(inverse(gt[t - 1]), gt[t]), 5.0, 5.0)
+        T_init = compose(P_prev, rel)
+        r = run_track(pft, vol, depth, intr, T_init, pst, params)
+        o = ov.track(depth, intr, T_init, pst, params)
+        assert_trace_parity(r["trace"], o["trace"], f"frame {t}")
+        P_prev = o["T"]
+        vol.integrate(T(depth), intr, T(P_prev))
+        ov.integrate(depth, intr, P_prev)
+        V, W = [x.cpu().numpy() for x in vol.download()]
+        assert np.array_equal(storage_bits(V), storage_bits(ov.V)), f"frame {t}: values differ"
+        assert np.array_equal(storage_bits(W), storage_bits(ov.W)), f"frame {t}: weights differ"
+    vol.close()
