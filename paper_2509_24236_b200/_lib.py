@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpft.so")
+LIB_PATH = os.environ.get("PFT_LIB") or os.path.join(HERE, "libpft.so")
 TRACE_DOUBLES = 24
 INTEGRATE_FULL_SWEEP = 1
 

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -73,7 +74,18 @@ void prof_begin(int cls, cudaStream_t st) {
   cudaEventRecord(t_open, st);
 }
 
-void prof_end(int cls, cudaStream_t st) {
+// PFT_SYNC_DEBUG=1: synchronise after every launch and name the kernel that failed (stderr).
+static const bool g_sync_debug = [] {
+  const char* e = getenv("PFT_SYNC_DEBUG");
+  return e && e[0] == '1';
+}();
+
+void prof_end(int cls, cudaStream_t st, const char* what) {
+  if (g_sync_debug) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "pft: launch failed (%s): %.160s\n", cudaGetErrorString(e), what);
+  }
   if (!g_prof_on.load(std::memory_order_relaxed) || !t_open) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t b = ev_get();
@@ -117,7 +129,7 @@ pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t 
   if (!n || !vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator not initialised");
   prof_begin(PFT_PROF_COMM, st);
   ncclResult_t r = n->allGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)vol->nccl_comm, st);
-  prof_end(PFT_PROF_COMM, st);
+  prof_end(PFT_PROF_COMM, st, "ncclAllGather");
   if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclAllGather: %s", n->errStr(r));
   return PFT_OK;
 }

@@ -203,6 +203,7 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
     else
       PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<__half><<<grid, 256, 0, st>>>(g, K, depth, T, (__half*)(vol->base + vol->L.v_off),
                                                       (__half*)(vol->base + vol->L.w_off), n));
+    records_rebuild_all(vol, st);
     return cuda_check("integrate (full sweep)");
   }
   uint32_t* tiles = (uint32_t*)(vol->base + vol->L.tiles_off);
@@ -223,6 +224,7 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   else
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (__half*)(vol->base + vol->L.v_off),
                                                    (__half*)(vol->base + vol->L.w_off)));
+  records_rebuild_list(vol, list, count, st);
   return cuda_check("integrate");
 }
 

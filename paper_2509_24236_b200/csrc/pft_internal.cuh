@@ -30,10 +30,19 @@ __host__ __device__ __forceinline__ uint32_t offx(int x) { return ((uint32_t)(x 
 __host__ __device__ __forceinline__ uint32_t offy(int y, uint32_t sy) { return (uint32_t)(y >> 2) * sy + ((uint32_t)(y & 3) << 2); }
 __host__ __device__ __forceinline__ uint32_t offz(int z, uint32_t sz) { return (uint32_t)(z >> 2) * sz + ((uint32_t)(z & 3) << 4); }
 
+// Cell records: the tracker reads, for trilinear cell (cx,cy,cz), its 8 corner
+// values as ONE 32-byte (fp32) / 16-byte (fp16) record [v000 v100 v010 v110 v001 v101 v011 v111]
+// at record index offx(cx)+offy(cy)+offz(cz) (same brick order as the voxels).  Records are
+// exact copies of the stored values, rebuilt by the fusion step for every touched brick.
+// Beside them, a 1-bit-per-cell in-band mask (bit w of the brick's uint64, w = cell index inside
+// the brick) says whether all 8 corners have |V| < 1 (reading L3); the tracker loads a record
+// only for in-band cells, so its working set is the band, not the search volume.
 // Byte layout of the caller-owned volume storage.
 struct VolLayout {
   size_t scratch_off, scratch_bytes;  // checksum / counters
   size_t v_off, w_off, elems;         // elems = nbx*nby*nbz*64 per array
+  size_t r_off;                       // cell records: elems x 8 values
+  size_t m_off;                       // in-band mask: one uint64 per brick, bit w = cell w
   size_t list_off, list_bytes;        // integration: active brick list (uint32 per brick)
   size_t tiles_off, tiles_bytes;      // integration: per-tile depth max (float)
   size_t total;
@@ -101,12 +110,16 @@ pft_status fail(pft_status s, const char* fmt, ...);
 pft_status cuda_check(const char* what);
 // Launch instrumentation (abi.cu): call prof_begin before and prof_end after each launch.
 void prof_begin(int cls, cudaStream_t st);
-void prof_end(int cls, cudaStream_t st);
+void prof_end(int cls, cudaStream_t st, const char* what);
+// Cell-record maintenance (volume.cu): rebuild every record, or those of the listed bricks
+// (cells [4b-1, 4b+3] per axis, i.e. every cell with a corner in the brick).
+void records_rebuild_all(pft_volume* vol, cudaStream_t st);
+void records_rebuild_list(pft_volume* vol, const uint32_t* list, const uint32_t* count, cudaStream_t st);
 #define PFT_LAUNCH(cls, st, ...)        \
   do {                                  \
     ::pft::prof_begin((cls), (st));     \
     __VA_ARGS__;                        \
-    ::pft::prof_end((cls), (st));       \
+    ::pft::prof_end((cls), (st), #__VA_ARGS__); \
   } while (0)
 // Validation helpers shared by the entry points.
 pft_status check_intrinsics(const pft_intrinsics* K);

@@ -16,19 +16,19 @@
 // fixed-point integers (2^-29) so per-particle totals are exact and independent of order,
 // CTA shape and sharding.
 #include <cmath>
+#include <cstdlib>
 
 #include "pft_internal.cuh"
 
 namespace pft {
 
 constexpr int kThreads = 256;  // 8 warps
-constexpr int kPPT = 2;        // points per thread (one 8x4 tile per warp per p)
+constexpr int kPPT = 4;        // points per thread in k_particle_eval (one 8x4 tile per warp per p)
+constexpr int kCentrePPT = 1;  // points per thread in k_centre (latency-bound: more CTAs)
 constexpr int kPC = 32;        // particles per CTA chunk
-constexpr int kPointsPerCTA = kThreads * kPPT;
 constexpr double kFixScale = 536870912.0;            // 2^29
 constexpr double kFixInv = 1.0 / 536870912.0;        // 2^-29
 
-struct Pose12 { double m[12]; };  // folded: g = M p + c, rows [M00 M01 M02 c0 | ...]
 
 // ------------------------------------------------------------------ pose algebra (fp64)
 // Rodrigues (reading L9): dR = I + (sin th/th)[r]x + ((1-cos th)/th^2)[r]x^2, th < 1e-12: I + [r]x.
@@ -116,55 +116,135 @@ __device__ __forceinline__ void template_delta(const float* __restrict__ a, doub
 }
 
 // ------------------------------------------------------------------ the gather-and-lerp core
-template <typename T> __device__ __forceinline__ float ldv(const T* p);
-template <> __device__ __forceinline__ float ldv<float>(const float* p) { return __ldg(p); }
-template <> __device__ __forceinline__ float ldv<__half>(const __half* p) { return __half2float(__ldg(p)); }
-
-// One particle-point evaluation (O3/O4): returns true and adds |v| to sum if the point is in band.
-template <typename T>
-__device__ __forceinline__ void eval_point(const T* __restrict__ V, const Geom& g, const double* m, double px,
-                                           double py, double pz, float& sum, unsigned& cnt) {
-  const double gx = fma(m[0], px, fma(m[1], py, fma(m[2], pz, m[3])));
-  const double gy = fma(m[4], px, fma(m[5], py, fma(m[6], pz, m[7])));
-  const double gz = fma(m[8], px, fma(m[9], py, fma(m[10], pz, m[11])));
-  const double flx = floor(gx), fly = floor(gy), flz = floor(gz);
-  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;  // saturating; finite by fold_pose
-  if ((unsigned)ix > (unsigned)(g.nx - 2) || (unsigned)iy > (unsigned)(g.ny - 2) || (unsigned)iz > (unsigned)(g.nz - 2))
-    return;
-  const float fx = (float)(gx - flx), fy = (float)(gy - fly), fz = (float)(gz - flz);
-  const uint32_t x0 = offx(ix), x1 = offx(ix + 1);
-  const uint32_t y0 = offy(iy, g.sy), y1 = offy(iy + 1, g.sy);
-  const uint32_t z0 = offz(iz, g.sz), z1 = offz(iz + 1, g.sz);
-  const float v000 = ldv(V + (x0 + y0 + z0)), v100 = ldv(V + (x1 + y0 + z0));
-  const float v010 = ldv(V + (x0 + y1 + z0)), v110 = ldv(V + (x1 + y1 + z0));
-  const float v001 = ldv(V + (x0 + y0 + z1)), v101 = ldv(V + (x1 + y0 + z1));
-  const float v011 = ldv(V + (x0 + y1 + z1)), v111 = ldv(V + (x1 + y1 + z1));
-  // in band iff all 8 corners |V| < 1 (reading L3)
-  const float amax = fmaxf(fmaxf(fmaxf(fabsf(v000), fabsf(v100)), fmaxf(fabsf(v010), fabsf(v110))),
-                           fmaxf(fmaxf(fabsf(v001), fabsf(v101)), fmaxf(fabsf(v011), fabsf(v111))));
-  if (!(amax < 1.0f)) return;
-  const float c00 = fmaf(fx, v100 - v000, v000), c10 = fmaf(fx, v110 - v010, v010);
-  const float c01 = fmaf(fx, v101 - v001, v001), c11 = fmaf(fx, v111 - v011, v011);
-  const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
-  const float val = fmaf(fz, c1 - c0, c0);
-  sum += fabsf(val);
-  cnt += 1u;
+// One 256-bit (fp32) / 128-bit (fp16) load per evaluation: the cell record of the 8 corners.
+__device__ __forceinline__ void ld_rec(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_rec(const __half* p, float (&v)[8]) {
+  // Two 64-bit loads: the single 128-bit form (ld.global[.nc].v4.b32) raised "misaligned address"
+  // in the <__half, 4> specialisation on B200 although the address is base + 16*o with a
+  // 4 KB-aligned base (cuda-gdb errorpc on the LDG.E.128; A/B in DESIGN.md §9).
+  unsigned u0, u1, u2, u3;
+  asm("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(u0), "=r"(u1) : "l"(p));
+  asm("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(u2), "=r"(u3) : "l"(p + 4));
+  const unsigned u[4] = {u0, u1, u2, u3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __half2float(__ushort_as_half((unsigned short)(u[i] & 0xffffu)));
+    v[2 * i + 1] = __half2float(__ushort_as_half((unsigned short)(u[i] >> 16)));
+  }
 }
 
-// Warp total of (sum, cnt) -> lane 0's fixed-point total.  All 32 lanes must call.
+// Cell index and fraction of grid coordinate g: n = floor(g), f = g - n (exact in fp64, then
+// rounded to fp32 for the lerp).  FAST (|g| < 2^30 guaranteed by the caller's bound):
+// t = g + 1.5*2^52 rounded toward -inf holds floor(g) in its low 32 bits and t - 1.5*2^52 is
+// floor(g) exactly, so the decision is the exact floor with three DADDs and no conversion-pipe
+// (XU) instruction.  Otherwise: FRND.FLOOR + saturating F2I.
+template <bool FAST>
+__device__ __forceinline__ int cell_split(double g, float& f) {
+  if (FAST) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dadd_rd(g, M);
+    f = __double2float_rn(__dsub_rn(g, __dsub_rn(t, M)));
+    return __double2loint(t);
+  } else {
+    const double fl = floor(g);
+    f = __double2float_rn(g - fl);
+    return (int)fl;  // saturates; finite by fold_pose
+  }
+}
+
+// PPT particle-point evaluations (O3/O4) of one pose, batched so the loads of all PPT points are
+// in flight together: (1) transforms, cell splits and bounds; (2) the in-band mask words;
+// (3) the 32-byte records, out-of-band lanes reading record 0 (one broadcast sector) instead
+// of branching; (4) trilinear lerps.  In-band points add |v| to sum and 1 to cnt.
+template <typename T, bool FAST, int PPT>
+__device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsigned long long* __restrict__ mask,
+                                            const Geom& g, const double (&m)[12], const double (&px)[PPT],
+                                            const double (&py)[PPT], const double (&pz)[PPT], float& sum,
+                                            unsigned& cnt) {
+  uint32_t o[PPT];
+  float fx[PPT], fy[PPT], fz[PPT];
+  bool ok[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const double gx = fma(m[0], px[p], fma(m[1], py[p], fma(m[2], pz[p], m[3])));
+    const double gy = fma(m[4], px[p], fma(m[5], py[p], fma(m[6], pz[p], m[7])));
+    const double gz = fma(m[8], px[p], fma(m[9], py[p], fma(m[10], pz[p], m[11])));
+    const int ix = cell_split<FAST>(gx, fx[p]), iy = cell_split<FAST>(gy, fy[p]), iz = cell_split<FAST>(gz, fz[p]);
+    ok[p] = pz[p] != 0.0 && (unsigned)ix <= (unsigned)(g.nx - 2) && (unsigned)iy <= (unsigned)(g.ny - 2) &&
+            (unsigned)iz <= (unsigned)(g.nz - 2);
+    o[p] = ok[p] ? offx(ix) + offy(iy, g.sy) + offz(iz, g.sz) : 0u;
+  }
+  // in band iff all 8 corners |V| < 1 (reading L3): one bit per cell, precomputed from the
+  // same stored values by the record builder
+  unsigned long long mw[PPT];
+#ifdef PFT_DEBUG
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const size_t nrec = (size_t)g.sz * (size_t)g.nbz;
+    if (o[p] >= nrec || ((uintptr_t)(mask + (o[p] >> 6)) & 7) || ((uintptr_t)(R + (size_t)o[p] * 8) & (8 * sizeof(T) - 1))) {
+      printf("pft debug: bad address p=%d o=%u nrec=%zu mask=%p R=%p ok=%d\n", p, o[p], nrec, (void*)mask, (void*)R, (int)ok[p]);
+      __trap();
+    }
+  }
+#endif
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) mw[p] = __ldg(mask + (o[p] >> 6));
+  float v[PPT][8];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    ok[p] = ok[p] && ((mw[p] >> (o[p] & 63)) & 1ull);
+    ld_rec(R + (size_t)(ok[p] ? o[p] : 0u) * 8, v[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const float c00 = fmaf(fx[p], v[p][1] - v[p][0], v[p][0]), c10 = fmaf(fx[p], v[p][3] - v[p][2], v[p][2]);
+    const float c01 = fmaf(fx[p], v[p][5] - v[p][4], v[p][4]), c11 = fmaf(fx[p], v[p][7] - v[p][6], v[p][6]);
+    const float c0 = fmaf(fy[p], c10 - c00, c00), c1 = fmaf(fy[p], c11 - c01, c01);
+    const float val = fmaf(fz[p], c1 - c0, c0);
+    sum += ok[p] ? fabsf(val) : 0.f;
+    cnt += ok[p] ? 1u : 0u;
+  }
+}
+
+// Warp total of (sum, cnt) -> fixed-point total (same value in every lane).  All lanes must call.
 __device__ __forceinline__ void warp_total(float sum, unsigned cnt, unsigned long long& S, unsigned& n) {
-  const unsigned fix = __float2uint_rn(sum * (float)kFixScale);  // sum < kPPT <= 7 -> < 2^32
+  const unsigned fix = __float2uint_rn(sum * (float)kFixScale);  // sum < kPPTmax = 7 -> < 2^32
   const unsigned lo = __reduce_add_sync(0xffffffffu, fix & 0xffffu);
   const unsigned hi = __reduce_add_sync(0xffffffffu, fix >> 16);
   n = __reduce_add_sync(0xffffffffu, cnt);
   S = ((unsigned long long)hi << 16) + lo;
 }
 
+// FAST-path bound for pose m on points with max |coordinate| <= pmax: every |g| < 2^30.
+__device__ __forceinline__ bool fast_ok(const double m[12], double pmax) {
+  bool ok = true;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    ok = ok && (fabs(m[4 * r]) + fabs(m[4 * r + 1]) + fabs(m[4 * r + 2])) * pmax + fabs(m[4 * r + 3]) < 1073741824.0;
+  return ok;
+}
+
 struct Points { const double *x, *y, *z; int npad; };
+
+// Block-wide max of v (blockDim.x == kThreads); all threads get the result.
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int s = 16; s > 0; s >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, s));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+#pragma unroll
+  for (int w = 1; w < kThreads / 32; ++w) r = fmax(r, red[w]);
+  return r;
+}
 
 // ------------------------------------------------------------------ kernels
 struct EvalArgs {
-  const void* V;
+  const void* R;             // cell records
+  const unsigned long long* mask;  // in-band bits
   Geom g;
   Points pts;
   int mode;                  // 0: template particles, 1: explicit poses
@@ -176,65 +256,81 @@ struct EvalArgs {
   PartRec* acc;              // indexed by k - k_begin
 };
 
-template <typename T>
-__global__ __launch_bounds__(kThreads, 3) void k_particle_eval(EvalArgs a) {
-  __shared__ __align__(16) double sPose[kPC][12];
+template <typename T, int PPT, bool FAST>
+__device__ __forceinline__ void eval_chunk(const EvalArgs& a, const double2 (*sPose)[6], const int* sFlag,
+                                          unsigned long long* sS, unsigned* sN, int kc, const double (&px)[PPT],
+                                          const double (&py)[PPT], const double (&pz)[PPT]) {
+  const T* R = (const T*)a.R;
+  for (int j = 0; j < kc; ++j) {
+    if (sFlag[j] != (FAST ? 2 : 1)) continue;  // block-uniform
+    double m[12];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const double2 q = sPose[j][i];
+      m[2 * i] = q.x;
+      m[2 * i + 1] = q.y;
+    }
+    float sum = 0.f;
+    unsigned cnt = 0u;
+    eval_points<T, FAST, PPT>(R, a.mask, a.g, m, px, py, pz, sum, cnt);
+    unsigned long long S;
+    unsigned n;
+    warp_total(sum, cnt, S, n);
+    if ((threadIdx.x & 31) == 0 && n) {
+      atomicAdd(&sS[j], S);
+      atomicAdd(&sN[j], n);
+    }
+  }
+}
+
+// a3/a4: CTA = kThreads x PPT points (PPT 8x4-pixel tiles per warp) x kPC particles.
+template <typename T, int PPT>
+__global__ __launch_bounds__(kThreads, 2) void k_particle_eval(EvalArgs a) {
+  __shared__ double2 sPose[kPC][6];
   __shared__ unsigned long long sS[kPC];
   __shared__ unsigned sN[kPC];
-  __shared__ int sOk[kPC];
+  __shared__ int sFlag[kPC];  // 0 invalid pose, 1 general path, 2 fast path
+  __shared__ double sRed[kThreads / 32];
   const int c0 = blockIdx.y * kPC;
   const int kc = min(kPC, a.k_count - c0);
   const int tid = threadIdx.x;
-  if (tid < kc) {
-    const int k = a.k_begin + c0 + tid;
-    double T[12];
-    if (a.mode == 0) {
-      double r[3], u[3], dR[9];
-      template_delta(a.pst + 6 * (size_t)k, a.st->omega, a.st->v, r, u);
-      rodrigues(r, dR);
-      apply_delta(dR, u, a.st->P, a.conv, T);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 12; ++i) T[i] = a.poses[12 * (size_t)k + i];
-    }
-    double m[12];
-    sOk[tid] = fold_pose(T, a.g, m);
-#pragma unroll
-    for (int i = 0; i < 12; ++i) sPose[tid][i] = m[i];
-    sS[tid] = 0ull;
-    sN[tid] = 0u;
-  }
   // this thread's points (8x4 tiles; z == 0 marks an invalid / padding slot)
-  double px[kPPT], py[kPPT], pz[kPPT];
+  double px[PPT], py[PPT], pz[PPT];
+  double pm = 0.0;
 #pragma unroll
-  for (int p = 0; p < kPPT; ++p) {
-    const int i = (blockIdx.x * kPPT + p) * kThreads + tid;
+  for (int p = 0; p < PPT; ++p) {
+    const int i = (blockIdx.x * PPT + p) * kThreads + tid;
     if (i < a.pts.npad) {
       px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i];
     } else {
       px[p] = py[p] = pz[p] = 0.0;
     }
+    pm = fmax(pm, fmax(fabs(px[p]), fmax(fabs(py[p]), fabs(pz[p]))));
+  }
+  const double pmax = block_max(pm, sRed);
+  if (tid < kc) {
+    const int k = a.k_begin + c0 + tid;
+    double T_[12];
+    if (a.mode == 0) {
+      double r[3], u[3], dR[9];
+      template_delta(a.pst + 6 * (size_t)k, a.st->omega, a.st->v, r, u);
+      rodrigues(r, dR);
+      apply_delta(dR, u, a.st->P, a.conv, T_);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 12; ++i) T_[i] = a.poses[12 * (size_t)k + i];
+    }
+    double m[12];
+    const bool ok = fold_pose(T_, a.g, m);
+    sFlag[tid] = !ok ? 0 : (fast_ok(m, pmax) ? 2 : 1);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sPose[tid][i] = make_double2(m[2 * i], m[2 * i + 1]);
+    sS[tid] = 0ull;
+    sN[tid] = 0u;
   }
   __syncthreads();
-  const T* V = (const T*)a.V;
-  for (int j = 0; j < kc; ++j) {
-    if (!sOk[j]) continue;  // block-uniform
-    double m[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) m[i] = sPose[j][i];
-    float sum = 0.f;
-    unsigned cnt = 0u;
-#pragma unroll
-    for (int p = 0; p < kPPT; ++p)
-      if (pz[p] != 0.0) eval_point<T>(V, a.g, m, px[p], py[p], pz[p], sum, cnt);
-    unsigned long long S;
-    unsigned n;
-    warp_total(sum, cnt, S, n);
-    if ((tid & 31) == 0 && n) {
-      atomicAdd(&sS[j], S);
-      atomicAdd(&sN[j], n);
-    }
-  }
+  eval_chunk<T, PPT, true>(a, sPose, sFlag, sS, sN, kc, px, py, pz);
+  eval_chunk<T, PPT, false>(a, sPose, sFlag, sS, sN, kc, px, py, pz);
   __syncthreads();
   if (tid < kc && sN[tid]) {
     PartRec* r = a.acc + (c0 + tid);
@@ -310,7 +406,8 @@ __global__ void k_backproject(BPArgs a) {
 
 // a5 + a8: E(P) of the current pose; the last CTA closes the iteration (s-law, trace).
 struct CentreArgs {
-  const void* V;
+  const void* R;
+  const unsigned long long* mask;
   Geom g;
   Points pts;
   TrackState* st;
@@ -325,14 +422,25 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
   __shared__ double sm[12];
   __shared__ int sOk;
   __shared__ bool sLast;
+  __shared__ double sRed[kThreads / 32];
   TrackState* st = a.st;
   const bool do_eval = a.initial || st->nA > 0;
   const int tid = threadIdx.x;
   if (do_eval) {
+    double px[kCentrePPT], py[kCentrePPT], pz[kCentrePPT], pm = 0.0;
+#pragma unroll
+    for (int p = 0; p < kCentrePPT; ++p) {
+      const int i = (blockIdx.x * kCentrePPT + p) * kThreads + tid;
+      px[p] = py[p] = pz[p] = 0.0;
+      if (i < a.pts.npad) { px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i]; }
+      pm = fmax(pm, fmax(fabs(px[p]), fmax(fabs(py[p]), fabs(pz[p]))));
+    }
+    const double pmax = block_max(pm, sRed);
     if (tid == 0) {
       double P[12], m[12];
       for (int i = 0; i < 12; ++i) P[i] = st->P[i];
-      sOk = fold_pose(P, a.g, m);
+      const bool ok = fold_pose(P, a.g, m);
+      sOk = !ok ? 0 : (fast_ok(m, pmax) ? 2 : 1);
       for (int i = 0; i < 12; ++i) sm[i] = m[i];
     }
     __syncthreads();
@@ -342,14 +450,8 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
       double m[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) m[i] = sm[i];
-#pragma unroll
-      for (int p = 0; p < kPPT; ++p) {
-        const int i = (blockIdx.x * kPPT + p) * kThreads + tid;
-        if (i < a.pts.npad) {
-          const double z = a.pts.z[i];
-          if (z != 0.0) eval_point<T>((const T*)a.V, a.g, m, a.pts.x[i], a.pts.y[i], z, sum, cnt);
-        }
-      }
+      if (sOk == 2) eval_points<T, true, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+      else eval_points<T, false, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
     }
     unsigned long long S;
     unsigned n;
@@ -548,8 +650,8 @@ static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_in
 
 template <typename T>
 static void launch_centre(const Launch& c, int initial, double beta, double rho, double* trace, double* T_out) {
-  CentreArgs ca{c.vol->base + c.vol->L.v_off, c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
-  int grid = (c.L.npad + kPointsPerCTA - 1) / kPointsPerCTA;
+  CentreArgs ca{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
+  int grid = (c.L.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
   PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
 }
 
@@ -557,9 +659,18 @@ template <typename T>
 static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin, int k_count, int conv,
                         const double* poses, PartRec* acc) {
   if (k_count <= 0) return;
-  EvalArgs ea{c.vol->base + c.vol->L.v_off, c.vol->g, c.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
-  dim3 grid((c.L.npad + kPointsPerCTA - 1) / kPointsPerCTA, (k_count + kPC - 1) / kPC);
-  PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T><<<grid, kThreads, 0, c.st>>>(ea));
+  EvalArgs ea{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
+  dim3 grid((c.L.npad + kThreads * kPPT - 1) / (kThreads * kPPT), (k_count + kPC - 1) / kPC);
+  static const int ppt = [] {  // tuning knob for experiments: PFT_EVAL_PPT=2|4
+    const char* e = getenv("PFT_EVAL_PPT");
+    return e && atoi(e) == 2 ? 2 : kPPT;
+  }();
+  if (ppt == 2) {
+    grid.x = (c.L.npad + kThreads * 2 - 1) / (kThreads * 2);
+    PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, 2><<<grid, kThreads, 0, c.st>>>(ea));
+  } else {
+    PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, kPPT><<<grid, kThreads, 0, c.st>>>(ea));
+  }
 }
 
 template <typename T>

@@ -46,6 +46,8 @@ static pft_status make_layout(const pft_volume_desc* d, Geom* g, VolLayout* L, s
   L->scratch_off = off; L->scratch_bytes = 4096; off += 4096;
   L->v_off = off; L->elems = elems; off = align_up(off + elems * *esize, 256);
   L->w_off = off; off = align_up(off + elems * *esize, 256);
+  L->r_off = off; off = align_up(off + elems * 8 * *esize, 256);
+  L->m_off = off; off = align_up(off + nb * 8, 256);
   L->list_off = off; L->list_bytes = nb * 4; off = align_up(off + L->list_bytes, 256);
   L->tiles_off = off; L->tiles_bytes = 64 * 1024 * 4; off = align_up(off + L->tiles_bytes, 256);
   L->total = off;
@@ -63,6 +65,91 @@ __global__ void k_reset(T* __restrict__ V, T* __restrict__ W, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     V[i] = one;
     W[i] = zero;
+  }
+}
+
+template <typename T>
+__global__ void k_fill(T* __restrict__ R, size_t n, float val) {
+  const T v = from_double<T>((double)val);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) R[i] = v;
+}
+
+// Record of cell (cx,cy,cz): its 8 corner values, x fastest (exact copies of stored bits).
+template <typename T> __device__ __forceinline__ float tof(T x);
+template <> __device__ __forceinline__ float tof<float>(float x) { return x; }
+template <> __device__ __forceinline__ float tof<__half>(__half x) { return __half2float(x); }
+
+// Writes the record of cell (cx,cy,cz); returns whether the cell is in band (all |V| < 1).
+template <typename T>
+__device__ __forceinline__ bool build_record(const Geom& g, const T* __restrict__ V, T* __restrict__ R, int cx, int cy,
+                                             int cz) {
+  const uint32_t x0 = offx(cx), x1 = offx(cx + 1), y0 = offy(cy, g.sy), y1 = offy(cy + 1, g.sy);
+  const uint32_t z0 = offz(cz, g.sz), z1 = offz(cz + 1, g.sz);
+  T r[8] = {V[x0 + y0 + z0], V[x1 + y0 + z0], V[x0 + y1 + z0], V[x1 + y1 + z0],
+            V[x0 + y0 + z1], V[x1 + y0 + z1], V[x0 + y1 + z1], V[x1 + y1 + z1]};
+  T* dst = R + (size_t)(x0 + y0 + z0) * 8;
+  if (sizeof(T) == 4) {
+    float4* d = (float4*)dst;
+    d[0] = make_float4(*(float*)&r[0], *(float*)&r[1], *(float*)&r[2], *(float*)&r[3]);
+    d[1] = make_float4(*(float*)&r[4], *(float*)&r[5], *(float*)&r[6], *(float*)&r[7]);
+  } else {
+    uint4 u;
+    u.x = (uint32_t)*(unsigned short*)&r[0] | ((uint32_t)*(unsigned short*)&r[1] << 16);
+    u.y = (uint32_t)*(unsigned short*)&r[2] | ((uint32_t)*(unsigned short*)&r[3] << 16);
+    u.z = (uint32_t)*(unsigned short*)&r[4] | ((uint32_t)*(unsigned short*)&r[5] << 16);
+    u.w = (uint32_t)*(unsigned short*)&r[6] | ((uint32_t)*(unsigned short*)&r[7] << 16);
+    *(uint4*)dst = u;
+  }
+  bool in = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) in = in && fabsf(tof<T>(r[i])) < 1.0f;
+  return in;
+}
+
+// Every cell: one thread per brick element (cells beyond n-2 are never read and are skipped).
+// Every cell: one thread per brick element; a warp covers half a brick, so the two 32-bit
+// halves of each brick's mask word are written by ballots without atomics.
+template <typename T>
+__global__ void k_records_all(Geom g, const T* __restrict__ V, T* __restrict__ R, uint32_t* __restrict__ mask,
+                              size_t nelem) {
+  for (size_t e0 = blockIdx.x * (size_t)blockDim.x; e0 < nelem; e0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = e0 + threadIdx.x;
+    bool in = false;
+    if (e < nelem) {
+      const uint32_t b = (uint32_t)(e >> 6), w = (uint32_t)(e & 63);
+      const int bx = (int)(b % (uint32_t)g.nbx);
+      const uint32_t r = b / (uint32_t)g.nbx;
+      const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+      const int cx = bx * 4 + (int)(w & 3), cy = by * 4 + (int)((w >> 2) & 3), cz = bz * 4 + (int)(w >> 4);
+      if (cx <= g.nx - 2 && cy <= g.ny - 2 && cz <= g.nz - 2) in = build_record<T>(g, V, R, cx, cy, cz);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if ((threadIdx.x & 31) == 0 && e < nelem) mask[e >> 5] = bal;
+  }
+}
+
+// Listed bricks: the 5^3 cells [4b-1, 4b+3] per axis whose corners include a voxel of brick b.
+// Neighbouring listed bricks rebuild shared apron cells with identical values (benign).
+template <typename T>
+__global__ __launch_bounds__(128) void k_records_list(Geom g, const T* __restrict__ V, T* __restrict__ R,
+                                                      uint32_t* __restrict__ mask, const uint32_t* __restrict__ list,
+                                                      const uint32_t* __restrict__ count) {
+  const uint32_t n = *count;
+  const int t = threadIdx.x;
+  if (t >= 125) return;
+  const int dx = t % 5 - 1, dy = (t / 5) % 5 - 1, dz = t / 25 - 1;
+  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
+    const uint32_t b = list[li];
+    const int bx = (int)(b % (uint32_t)g.nbx);
+    const uint32_t r = b / (uint32_t)g.nbx;
+    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+    const int cx = bx * 4 + dx, cy = by * 4 + dy, cz = bz * 4 + dz;
+    if (cx < 0 || cy < 0 || cz < 0 || cx > g.nx - 2 || cy > g.ny - 2 || cz > g.nz - 2) continue;
+    const bool in = build_record<T>(g, V, R, cx, cy, cz);
+    const uint32_t o = offx(cx) + offy(cy, g.sy) + offz(cz, g.sz);
+    const uint32_t bit = 1u << (o & 31);
+    if (in) atomicOr(mask + (o >> 5), bit);
+    else atomicAnd(mask + (o >> 5), ~bit);
   }
 }
 
@@ -130,11 +217,31 @@ static int grid_for(size_t n, int threads) {
 
 pft_status volume_reset_impl(pft_volume* vol, cudaStream_t st) {
   size_t n = vol->L.elems;
-  if (vol->esize == 4)
+  if (vol->esize == 4) {
     PFT_LAUNCH(PFT_PROF_OTHER, st, k_reset<float><<<grid_for(n, 256), 256, 0, st>>>((float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.w_off), n));
-  else
+    PFT_LAUNCH(PFT_PROF_OTHER, st, k_fill<float><<<grid_for(8 * n, 256), 256, 0, st>>>((float*)(vol->base + vol->L.r_off), 8 * n, 1.0f));
+  } else {
     PFT_LAUNCH(PFT_PROF_OTHER, st, k_reset<__half><<<grid_for(n, 256), 256, 0, st>>>((__half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.w_off), n));
+    PFT_LAUNCH(PFT_PROF_OTHER, st, k_fill<__half><<<grid_for(8 * n, 256), 256, 0, st>>>((__half*)(vol->base + vol->L.r_off), 8 * n, 1.0f));
+  }
+  cudaMemsetAsync(vol->base + vol->L.m_off, 0, (n / 64) * 8, st);  // nothing is in band
   return cuda_check("volume_reset");
+}
+
+void records_rebuild_all(pft_volume* vol, cudaStream_t st) {
+  size_t n = vol->L.elems;
+  if (vol->esize == 4)
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_all<float><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
+  else
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_all<__half><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
+}
+
+void records_rebuild_list(pft_volume* vol, const uint32_t* list, const uint32_t* count, cudaStream_t st) {
+  const int grid = 148 * 16;
+  if (vol->esize == 4)
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_list<float><<<grid, 128, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), list, count));
+  else
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_list<__half><<<grid, 128, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), list, count));
 }
 
 }  // namespace pft
@@ -187,6 +294,7 @@ pft_status pft_volume_upload(pft_volume* vol, const void* dv, const void* dw, vo
   else
     PFT_LAUNCH(PFT_PROF_OTHER, st, k_upload<__half><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const __half*)dv, (const __half*)dw,
         (__half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.w_off), n));
+  records_rebuild_all(vol, st);
   return cuda_check("volume_upload");
 }
 
