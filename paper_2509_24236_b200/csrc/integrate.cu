@@ -29,8 +29,13 @@ template <typename T> __device__ __forceinline__ T store_rn(double x);
 template <> __device__ __forceinline__ float store_rn<float>(double x) { return __double2float_rn(x); }
 template <> __device__ __forceinline__ __half store_rn<__half>(double x) { return __double2half(x); }
 
+template <typename T> __device__ __forceinline__ bool same_bits(T a, T b);
+template <> __device__ __forceinline__ bool same_bits<float>(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+template <> __device__ __forceinline__ bool same_bits<__half>(__half a, __half b) { return __half_as_ushort(a) == __half_as_ushort(b); }
+
+// Returns true iff the stored value V changed (its cell records must then be refreshed).
 template <typename T>
-__device__ __forceinline__ void fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
+__device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
                                            const double* T_, int i, int j, int k, T* __restrict__ V,
                                            T* __restrict__ W, uint32_t o) {
   const double gw0 = __dadd_rn(g.ox, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
@@ -38,28 +43,31 @@ __device__ __forceinline__ void fuse_voxel(const Geom& g, const Intr& K, const u
   const double gw2 = __dadd_rn(g.oz, __dmul_rn(g.voxel, __dadd_rn((double)k, 0.5)));
   const double d0 = __dsub_rn(gw0, T_[3]), d1 = __dsub_rn(gw1, T_[7]), d2 = __dsub_rn(gw2, T_[11]);
   const double z = __dadd_rn(__dadd_rn(__dmul_rn(T_[2], d0), __dmul_rn(T_[6], d1)), __dmul_rn(T_[10], d2));
-  if (!(z > 0.0)) return;
+  if (!(z > 0.0)) return false;
   const double x = __dadd_rn(__dadd_rn(__dmul_rn(T_[0], d0), __dmul_rn(T_[4], d1)), __dmul_rn(T_[8], d2));
   const double y = __dadd_rn(__dadd_rn(__dmul_rn(T_[1], d0), __dmul_rn(T_[5], d1)), __dmul_rn(T_[9], d2));
   const double u = __dadd_rn(__ddiv_rn(__dmul_rn(K.fx, x), z), K.cx);
   const double uf = floor(__dadd_rn(u, 0.5));
-  if (!(uf >= 0.0 && uf < (double)K.W)) return;
+  if (!(uf >= 0.0 && uf < (double)K.W)) return false;
   const double v = __dadd_rn(__ddiv_rn(__dmul_rn(K.fy, y), z), K.cy);
   const double vf = floor(__dadd_rn(v, 0.5));
-  if (!(vf >= 0.0 && vf < (double)K.H)) return;
+  if (!(vf >= 0.0 && vf < (double)K.H)) return false;
   const uint16_t raw = __ldg(depth + (size_t)vf * K.W + (size_t)uf);
   const double d = __dmul_rn((double)raw, K.unit);
-  if (raw == 0 || !(d < g.max_depth)) return;
+  if (raw == 0 || !(d < g.max_depth)) return false;
   const double sdf = __dsub_rn(d, z);
-  if (!(sdf > -g.trunc)) return;
+  if (!(sdf > -g.trunc)) return false;
   double vnew = __ddiv_rn(sdf, g.trunc);
   if (vnew > 1.0) vnew = 1.0;
-  const double Vo = to_double<T>(V[o]), Wo = to_double<T>(W[o]);
+  const T Vs = V[o];
+  const double Vo = to_double<T>(Vs), Wo = to_double<T>(W[o]);
   const double Wp = __dadd_rn(Wo, 1.0);
   const double Vn = __ddiv_rn(__dadd_rn(__dmul_rn(Vo, Wo), vnew), Wp);
   const double Wn = Wp > g.max_weight ? g.max_weight : Wp;
-  V[o] = store_rn<T>(Vn);
+  const T Vnew = store_rn<T>(Vn);
+  V[o] = Vnew;
   W[o] = store_rn<T>(Wn);
+  return !same_bits<T>(Vs, Vnew);
 }
 
 // Full sweep: one thread per brick element (the verification path).
@@ -170,7 +178,8 @@ template <typename T>
 __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const uint16_t* __restrict__ depth,
                                                         const double* __restrict__ Tdev, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, T* __restrict__ V,
-                                                        T* __restrict__ W) {
+                                                        T* __restrict__ W, uint32_t* __restrict__ dirty,
+                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount) {
   __shared__ double sT[12];
   if (threadIdx.x < 12) sT[threadIdx.x] = Tdev[threadIdx.x];
   __syncthreads();
@@ -182,8 +191,19 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
     const uint32_t r = b / (uint32_t)g.nbx;
     const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
     const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
-    if (i >= g.nx || j >= g.ny || k >= g.nz) continue;
-    fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, b * 64u + w);
+    bool changed = false;
+    if (i < g.nx && j < g.ny && k < g.nz) changed = fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, b * 64u + w);
+    // cell-bricks whose records read this voxel: (b - d) for d in {0,1}^3, the -1 neighbours
+    // only from the brick's low faces
+    unsigned nbm = 0u;
+    if (changed) {
+      const unsigned ex = (w & 3) == 0, ey = ((w >> 2) & 3) == 0, ez = (w >> 4) == 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if ((!(q & 1) || ex) && (!(q & 2) || ey) && (!(q & 4) || ez)) nbm |= 1u << q;
+    }
+    nbm = __reduce_or_sync(0xffffffffu, nbm);
+    if ((threadIdx.x & 31) == 0 && nbm) mark_dirty_cells(g, bx, by, bz, nbm, dirty, dlist, dcount);
   }
 }
 
@@ -209,7 +229,10 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   uint32_t* tiles = (uint32_t*)(vol->base + vol->L.tiles_off);
   uint32_t* list = (uint32_t*)(vol->base + vol->L.list_off);
   uint32_t* count = (uint32_t*)(vol->base + vol->L.scratch_off + 64);
-  cudaMemsetAsync(count, 0, 4, st);
+  uint32_t* dcount = (uint32_t*)(vol->base + vol->L.scratch_off + 128);
+  uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
+  uint32_t* dlist = (uint32_t*)(vol->base + vol->L.dlist_off);
+  cudaMemsetAsync(count, 0, 128, st);  // active count and dirty count
   {
     dim3 blk(32, 8);
     int nt = ntx * nty;
@@ -220,11 +243,11 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   const int grid = 148 * 8;
   if (vol->esize == 4)
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (float*)(vol->base + vol->L.v_off),
-                                                  (float*)(vol->base + vol->L.w_off)));
+                                                  (float*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
   else
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (__half*)(vol->base + vol->L.v_off),
-                                                   (__half*)(vol->base + vol->L.w_off)));
-  records_rebuild_list(vol, list, count, st);
+                                                   (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
+  records_rebuild_dirty(vol, st);
   return cuda_check("integrate");
 }
 

@@ -44,6 +44,7 @@ struct VolLayout {
   size_t r_off;                       // cell records: elems x 8 values
   size_t m_off;                       // in-band mask: one uint64 per brick, bit w = cell w
   size_t list_off, list_bytes;        // integration: active brick list (uint32 per brick)
+  size_t dirty_off, dlist_off;        // records: dirty flag per cell-brick + dirty list (uint32 each)
   size_t tiles_off, tiles_bytes;      // integration: per-tile depth max (float)
   size_t total;
 };
@@ -114,7 +115,20 @@ void prof_end(int cls, cudaStream_t st, const char* what);
 // Cell-record maintenance (volume.cu): rebuild every record, or those of the listed bricks
 // (cells [4b-1, 4b+3] per axis, i.e. every cell with a corner in the brick).
 void records_rebuild_all(pft_volume* vol, cudaStream_t st);
-void records_rebuild_list(pft_volume* vol, const uint32_t* list, const uint32_t* count, cudaStream_t st);
+void records_rebuild_dirty(pft_volume* vol, cudaStream_t st);
+// Marks (dedup'ed) the cell-bricks whose records depend on voxel (x,y,z) of brick (bx,by,bz):
+// cells [x-1, x] per axis.  Called by the fusion kernel for voxels whose stored V changed.
+__device__ __forceinline__ void mark_dirty_cells(const Geom& g, int bx, int by, int bz, unsigned nbmask,
+                                                 uint32_t* dirty, uint32_t* dlist, uint32_t* dcount) {
+  // nbmask bit (dz*4 + dy*2 + dx): cell-brick (bx-dx, by-dy, bz-dz) is affected
+  for (int i = 0; i < 8; ++i) {
+    if (!((nbmask >> i) & 1u)) continue;
+    const int cx = bx - (i & 1), cy = by - ((i >> 1) & 1), cz = bz - (i >> 2);
+    if (cx < 0 || cy < 0 || cz < 0) continue;
+    const uint32_t cb = ((uint32_t)cz * g.nby + (uint32_t)cy) * g.nbx + (uint32_t)cx;
+    if (atomicExch(dirty + cb, 1u) == 0u) dlist[atomicAdd(dcount, 1u)] = cb;
+  }
+}
 #define PFT_LAUNCH(cls, st, ...)        \
   do {                                  \
     ::pft::prof_begin((cls), (st));     \

@@ -49,6 +49,8 @@ static pft_status make_layout(const pft_volume_desc* d, Geom* g, VolLayout* L, s
   L->r_off = off; off = align_up(off + elems * 8 * *esize, 256);
   L->m_off = off; off = align_up(off + nb * 8, 256);
   L->list_off = off; L->list_bytes = nb * 4; off = align_up(off + L->list_bytes, 256);
+  L->dirty_off = off; off = align_up(off + nb * 4, 256);
+  L->dlist_off = off; off = align_up(off + nb * 4, 256);
   L->tiles_off = off; L->tiles_bytes = 64 * 1024 * 4; off = align_up(off + L->tiles_bytes, 256);
   L->total = off;
   return PFT_OK;
@@ -128,28 +130,26 @@ __global__ void k_records_all(Geom g, const T* __restrict__ V, T* __restrict__ R
   }
 }
 
-// Listed bricks: the 5^3 cells [4b-1, 4b+3] per axis whose corners include a voxel of brick b.
-// Neighbouring listed bricks rebuild shared apron cells with identical values (benign).
+// Dirty cell-bricks: 64 threads (two warps) rebuild the brick's 64 cell records and write the
+// two 32-bit halves of its mask word by ballot; then the dirty flag is cleared.
 template <typename T>
-__global__ __launch_bounds__(128) void k_records_list(Geom g, const T* __restrict__ V, T* __restrict__ R,
-                                                      uint32_t* __restrict__ mask, const uint32_t* __restrict__ list,
-                                                      const uint32_t* __restrict__ count) {
-  const uint32_t n = *count;
-  const int t = threadIdx.x;
-  if (t >= 125) return;
-  const int dx = t % 5 - 1, dy = (t / 5) % 5 - 1, dz = t / 25 - 1;
-  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
-    const uint32_t b = list[li];
+__global__ __launch_bounds__(256) void k_records_dirty(Geom g, const T* __restrict__ V, T* __restrict__ R,
+                                                       uint32_t* __restrict__ mask, uint32_t* __restrict__ dirty,
+                                                       const uint32_t* __restrict__ dlist,
+                                                       const uint32_t* __restrict__ dcount) {
+  const uint32_t n = *dcount;
+  const uint32_t w = threadIdx.x & 63;
+  for (uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6); li < n; li += gridDim.x * 4) {
+    const uint32_t b = dlist[li];
     const int bx = (int)(b % (uint32_t)g.nbx);
     const uint32_t r = b / (uint32_t)g.nbx;
     const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
-    const int cx = bx * 4 + dx, cy = by * 4 + dy, cz = bz * 4 + dz;
-    if (cx < 0 || cy < 0 || cz < 0 || cx > g.nx - 2 || cy > g.ny - 2 || cz > g.nz - 2) continue;
-    const bool in = build_record<T>(g, V, R, cx, cy, cz);
-    const uint32_t o = offx(cx) + offy(cy, g.sy) + offz(cz, g.sz);
-    const uint32_t bit = 1u << (o & 31);
-    if (in) atomicOr(mask + (o >> 5), bit);
-    else atomicAnd(mask + (o >> 5), ~bit);
+    const int cx = bx * 4 + (int)(w & 3), cy = by * 4 + (int)((w >> 2) & 3), cz = bz * 4 + (int)(w >> 4);
+    bool in = false;
+    if (cx <= g.nx - 2 && cy <= g.ny - 2 && cz <= g.nz - 2) in = build_record<T>(g, V, R, cx, cy, cz);
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if ((threadIdx.x & 31) == 0) mask[b * 2 + (w >> 5)] = bal;
+    if (w == 0) dirty[b] = 0u;
   }
 }
 
@@ -225,23 +225,27 @@ pft_status volume_reset_impl(pft_volume* vol, cudaStream_t st) {
     PFT_LAUNCH(PFT_PROF_OTHER, st, k_fill<__half><<<grid_for(8 * n, 256), 256, 0, st>>>((__half*)(vol->base + vol->L.r_off), 8 * n, 1.0f));
   }
   cudaMemsetAsync(vol->base + vol->L.m_off, 0, (n / 64) * 8, st);  // nothing is in band
+  cudaMemsetAsync(vol->base + vol->L.dirty_off, 0, (n / 64) * 4, st);
   return cuda_check("volume_reset");
 }
 
 void records_rebuild_all(pft_volume* vol, cudaStream_t st) {
   size_t n = vol->L.elems;
   if (vol->esize == 4)
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_all<float><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_all<float><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
   else
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_all<__half><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_all<__half><<<grid_for(n, 256), 256, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), n));
 }
 
-void records_rebuild_list(pft_volume* vol, const uint32_t* list, const uint32_t* count, cudaStream_t st) {
-  const int grid = 148 * 16;
+void records_rebuild_dirty(pft_volume* vol, cudaStream_t st) {
+  const int grid = 148 * 8;
+  uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
+  const uint32_t* dlist = (const uint32_t*)(vol->base + vol->L.dlist_off);
+  const uint32_t* dcount = (const uint32_t*)(vol->base + vol->L.scratch_off + 128);
   if (vol->esize == 4)
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_list<float><<<grid, 128, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), list, count));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_dirty<float><<<grid, 256, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
   else
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_records_list<__half><<<grid, 128, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), list, count));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_dirty<__half><<<grid, 256, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
 }
 
 }  // namespace pft
