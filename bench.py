@@ -219,8 +219,12 @@ def run_ours(args):
     d2h = 96
 
     # ---- roofline of the dominant kernel (k_particle_eval)
-    eval_ms, eval_n = prof["eval"]
-    evals_per_launch = K_PER_GPU * statistics.mean(n_valid[i] for i in idx)
+    if prof["eval"][1] > 0:       # multi-launch tracker: k_particle_eval is the dominant kernel
+        kname, (eval_ms, eval_n) = "k_particle_eval", prof["eval"]
+        evals_per_launch = K_PER_GPU * statistics.mean(n_valid[i] for i in idx)
+    else:                         # persistent tracker: one launch per frame holds all 10 iterations
+        kname, (eval_ms, eval_n) = "k_track_persistent (eval+update+centre phases)", prof["track"]
+        evals_per_launch = K_PER_GPU * ITERS * statistics.mean(n_valid[i] for i in idx)
     avg_launch_s = eval_ms / eval_n * 1e-3
     achieved = evals_per_launch * BYTES_PER_EVAL / avg_launch_s / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -249,7 +253,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_particle_eval",
+                     "traffic": traffic, "kernel": kname,
                      "basis": f"{BYTES_PER_EVAL} B logical gather/eval x {evals_per_launch:.0f} evals/launch; "
                               "gathers are L2/L1-resident (DESIGN.md §7)",
                      "evals_per_s_kernel": evals_per_launch / avg_launch_s},

@@ -215,7 +215,8 @@ pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks,
 #define PFT_PROF_COMM 6        /* ncclAllGather (a6)                                          */
 #define PFT_PROF_OTHER 7       /* volume reset / upload / download / checksum                 */
 #define PFT_PROF_RECORDS 8     /* tracker cell-record / in-band-mask maintenance (a10)        */
-#define PFT_PROF_CLASSES 9
+#define PFT_PROF_TRACK 9       /* k_track_persistent: the whole RO loop in one launch (G = 1) */
+#define PFT_PROF_CLASSES 10
 
 /* Cumulative number of CUDA kernels (and NCCL collectives) this library has launched. */
 uint64_t pft_launch_count(void);

@@ -21,7 +21,7 @@ EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_vol
            "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
            "pft_comm_init", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
-PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records"]
+PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records", "track"]
 
 
 class PftError(RuntimeError):

@@ -89,7 +89,9 @@ struct TrackState {
   int Nvalid;          // valid strided points
   unsigned int ticket_upd, ticket_ctr;
   int pad0;
-  double pad[8];
+  unsigned long long pmax_bits;  // max |point coordinate| of the frame (fp64 bits; persistent path)
+  unsigned int bar_count, bar_gen;  // software grid barrier (persistent path)
+  double pad[6];
 };
 
 struct TrackLayout {
@@ -97,6 +99,9 @@ struct TrackLayout {
   size_t pts_off;      // 3 * npad doubles (x, y, z SoA)
   size_t acc_local_off, acc_full_off;
   size_t part_off;     // update partials: nblk_upd * 8 doubles
+  size_t ptab_off;     // persistent path: K x 12 folded candidate poses + K flags
+  size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
+  size_t work_off;     // persistent path: per-iteration work counters
   size_t total;
   int npad, ntx, nty, nr, nc;  // point slots, tiles, strided grid rows / cols
   int kloc, kfull, nblk_upd;

@@ -115,6 +115,68 @@ __device__ __forceinline__ void template_delta(const float* __restrict__ a, doub
   }
 }
 
+// ------------------------------------------------------------------ shared, non-inlined steps
+// Both tracker implementations (multi-launch and persistent) call these exact functions, so their
+// fp64 arithmetic (including FMA contraction) is identical and results are bit-identical.
+__device__ __forceinline__ bool fast_ok(const double m[12], double pmax);
+
+// a3: folded pose of candidate k = (dR_k R, t + u_k) (or world-literal) in grid coordinates.
+// Returns 0 (invalid pose), 1 (general floor path) or 2 (fast floor path, |g| < 2^30).
+__device__ __noinline__ int candidate_pose(const float* __restrict__ pst_row, double omega, double v, const double* P,
+                                           int conv, const Geom& g, double pmax, double* m) {
+  double r[3], u[3], dR[9], T_[12];
+  template_delta(pst_row, omega, v, r, u);
+  rodrigues(r, dR);
+  apply_delta(dR, u, P, conv, T_);
+  double mm[12];
+  const bool ok = fold_pose(T_, g, mm);
+  for (int i = 0; i < 12; ++i) m[i] = mm[i];
+  return !ok ? 0 : (fast_ok(mm, pmax) ? 2 : 1);
+}
+
+// Folded explicit pose (pft_eval_poses rows, and the centre pose P).
+__device__ __noinline__ int explicit_pose(const double* T_, const Geom& g, double pmax, double* m) {
+  double t[12], mm[12];
+  for (int i = 0; i < 12; ++i) t[i] = T_[i];
+  const bool ok = fold_pose(t, g, mm);
+  for (int i = 0; i < 12; ++i) m[i] = mm[i];
+  return !ok ? 0 : (fast_ok(mm, pmax) ? 2 : 1);
+}
+
+// a7: unit quaternion and translation of template row k at search size s (advantage-set member).
+__device__ __noinline__ void member_delta(const float* __restrict__ pst_row, double omega, double v, double* q,
+                                          double* u) {
+  double r[3], uu[3], qq[4];
+  template_delta(pst_row, omega, v, r, uu);
+  rotvec_quat(r, qq);
+  for (int i = 0; i < 4; ++i) q[i] = qq[i];
+  for (int i = 0; i < 3; ++i) u[i] = uu[i];
+}
+
+// a7: P <- (R(Q/|Q|), U/|A|) P, Q and U the sums over the advantage set.
+__device__ __noinline__ void apply_mean(const double* Q, const double* U, int nA, const double* P, int conv,
+                                        double* Pn) {
+  const double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
+  const double qb[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
+  const double ub[3] = {U[0] / nA, U[1] / nA, U[2] / nA};
+  double Rb[9], PP[12], out[12];
+  quat_to_R(qb, Rb);
+  for (int i = 0; i < 12; ++i) PP[i] = P[i];
+  apply_delta(Rb, ub, PP, conv, out);
+  for (int i = 0; i < 12; ++i) Pn[i] = out[i];
+}
+
+// 256-thread fixed-shape tree over red[8][256] (result in red[c][0]); all threads must call.
+__device__ __forceinline__ void tree8(double (*red)[256], int tid) {
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (tid < s)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ the gather-and-lerp core
 // One 256-bit (fp32) / 128-bit (fp16) load per evaluation: the cell record of the 8 corners.
 __device__ __forceinline__ void ld_rec(const float* p, float (&v)[8]) {
@@ -159,12 +221,15 @@ __device__ __forceinline__ int cell_split(double g, float& f) {
 // PPT particle-point evaluations (O3/O4) of one pose, batched so the loads of all PPT points are
 // in flight together: (1) transforms, cell splits and bounds; (2) the in-band mask words;
 // (3) the 32-byte records, out-of-band lanes reading record 0 (one broadcast sector) instead
-// of branching; (4) trilinear lerps.  In-band points add |v| to sum and 1 to cnt.
+// of branching; (4) trilinear lerps.  In-band points add round(|v| * 2^29) to fix and 1 to cnt:
+// each term is converted to fixed point on its own, so every sum is an exact integer whatever
+// the grouping of points into threads, warps, CTAs or ranks.
 template <typename T, bool FAST, int PPT>
 __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsigned long long* __restrict__ mask,
                                             const Geom& g, const double (&m)[12], const double (&px)[PPT],
-                                            const double (&py)[PPT], const double (&pz)[PPT], float& sum,
+                                            const double (&py)[PPT], const double (&pz)[PPT], unsigned& fix,
                                             unsigned& cnt) {
+  static_assert(PPT <= 7, "per-thread fixed-point sum must stay below 2^32");
   uint32_t o[PPT];
   float fx[PPT], fy[PPT], fz[PPT];
   bool ok[PPT];
@@ -205,14 +270,13 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
     const float c01 = fmaf(fx[p], v[p][5] - v[p][4], v[p][4]), c11 = fmaf(fx[p], v[p][7] - v[p][6], v[p][6]);
     const float c0 = fmaf(fy[p], c10 - c00, c00), c1 = fmaf(fy[p], c11 - c01, c01);
     const float val = fmaf(fz[p], c1 - c0, c0);
-    sum += ok[p] ? fabsf(val) : 0.f;
+    fix += ok[p] ? __float2uint_rn(fabsf(val) * (float)kFixScale) : 0u;
     cnt += ok[p] ? 1u : 0u;
   }
 }
 
-// Warp total of (sum, cnt) -> fixed-point total (same value in every lane).  All lanes must call.
-__device__ __forceinline__ void warp_total(float sum, unsigned cnt, unsigned long long& S, unsigned& n) {
-  const unsigned fix = __float2uint_rn(sum * (float)kFixScale);  // sum < kPPTmax = 7 -> < 2^32
+// Warp total of (fix, cnt) -> 64-bit fixed-point total (same value in every lane).  All lanes must call.
+__device__ __forceinline__ void warp_total(unsigned fix, unsigned cnt, unsigned long long& S, unsigned& n) {
   const unsigned lo = __reduce_add_sync(0xffffffffu, fix & 0xffffu);
   const unsigned hi = __reduce_add_sync(0xffffffffu, fix >> 16);
   n = __reduce_add_sync(0xffffffffu, cnt);
@@ -270,7 +334,7 @@ __device__ __forceinline__ void eval_chunk(const EvalArgs& a, const double2 (*sP
       m[2 * i] = q.x;
       m[2 * i + 1] = q.y;
     }
-    float sum = 0.f;
+    unsigned sum = 0u;
     unsigned cnt = 0u;
     eval_points<T, FAST, PPT>(R, a.mask, a.g, m, px, py, pz, sum, cnt);
     unsigned long long S;
@@ -285,7 +349,10 @@ __device__ __forceinline__ void eval_chunk(const EvalArgs& a, const double2 (*sP
 
 // a3/a4: CTA = kThreads x PPT points (PPT 8x4-pixel tiles per warp) x kPC particles.
 template <typename T, int PPT>
-__global__ __launch_bounds__(kThreads, 2) void k_particle_eval(EvalArgs a) {
+#ifndef PFT_MINB
+#define PFT_MINB 2
+#endif
+__global__ __launch_bounds__(kThreads, PFT_MINB) void k_particle_eval(EvalArgs a) {
   __shared__ double2 sPose[kPC][6];
   __shared__ unsigned long long sS[kPC];
   __shared__ unsigned sN[kPC];
@@ -310,19 +377,9 @@ __global__ __launch_bounds__(kThreads, 2) void k_particle_eval(EvalArgs a) {
   const double pmax = block_max(pm, sRed);
   if (tid < kc) {
     const int k = a.k_begin + c0 + tid;
-    double T_[12];
-    if (a.mode == 0) {
-      double r[3], u[3], dR[9];
-      template_delta(a.pst + 6 * (size_t)k, a.st->omega, a.st->v, r, u);
-      rodrigues(r, dR);
-      apply_delta(dR, u, a.st->P, a.conv, T_);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 12; ++i) T_[i] = a.poses[12 * (size_t)k + i];
-    }
     double m[12];
-    const bool ok = fold_pose(T_, a.g, m);
-    sFlag[tid] = !ok ? 0 : (fast_ok(m, pmax) ? 2 : 1);
+    sFlag[tid] = a.mode == 0 ? candidate_pose(a.pst + 6 * (size_t)k, a.st->omega, a.st->v, a.st->P, a.conv, a.g, pmax, m)
+                             : explicit_pose(a.poses + 12 * (size_t)k, a.g, pmax, m);
 #pragma unroll
     for (int i = 0; i < 6; ++i) sPose[tid][i] = make_double2(m[2 * i], m[2 * i + 1]);
     sS[tid] = 0ull;
@@ -437,14 +494,12 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
     }
     const double pmax = block_max(pm, sRed);
     if (tid == 0) {
-      double P[12], m[12];
-      for (int i = 0; i < 12; ++i) P[i] = st->P[i];
-      const bool ok = fold_pose(P, a.g, m);
-      sOk = !ok ? 0 : (fast_ok(m, pmax) ? 2 : 1);
+      double m[12];
+      sOk = explicit_pose(st->P, a.g, pmax, m);
       for (int i = 0; i < 12; ++i) sm[i] = m[i];
     }
     __syncthreads();
-    float sum = 0.f;
+    unsigned sum = 0u;
     unsigned cnt = 0u;
     if (sOk) {
       double m[12];
@@ -535,9 +590,7 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
     a.E_out[k] = E;
     a.n_out[k] = (int)rec.n;
     if (E < Ec) {
-      double r[3];
-      template_delta(a.pst + 6 * (size_t)k, st->omega, st->v, r, u);
-      rotvec_quat(r, q);
+      member_delta(a.pst + 6 * (size_t)k, st->omega, st->v, q, u);
       member = 1.0;
     }
     const int j = k - a.k_begin;
@@ -548,13 +601,7 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
   }
   red[0][tid] = q[0]; red[1][tid] = q[1]; red[2][tid] = q[2]; red[3][tid] = q[3];
   red[4][tid] = u[0]; red[5][tid] = u[1]; red[6][tid] = u[2]; red[7][tid] = member;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (tid < s)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
-    __syncthreads();
-  }
+  tree8(red, tid);
   if (tid < 8) a.partials[blockIdx.x * 8 + tid] = red[tid][0];
   __threadfence();
   __syncthreads();
@@ -568,13 +615,7 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
   for (int b = tid; b < (int)gridDim.x; b += 256)
 #pragma unroll
     for (int c = 0; c < 8; ++c) red[c][tid] += __ldcg(a.partials + b * 8 + c);
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (tid < s)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
-    __syncthreads();
-  }
+  tree8(red, tid);
   if (tid == 0) {
     const int nA = (int)red[7][0];
     st->nA = nA;
@@ -582,15 +623,323 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
     st->ticket_upd = 0u;
     if (nA > 0) {
       const double Q[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
-      const double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
-      const double qb[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
-      const double ub[3] = {red[4][0] / nA, red[5][0] / nA, red[6][0] / nA};
-      double Rb[9], P[12], Pn[12];
-      quat_to_R(qb, Rb);
-      for (int i = 0; i < 12; ++i) P[i] = st->P[i];
-      apply_delta(Rb, ub, P, a.conv, Pn);
+      const double U[3] = {red[4][0], red[5][0], red[6][0]};
+      double Pn[12];
+      apply_mean(Q, U, nA, st->P, a.conv, Pn);
       for (int i = 0; i < 12; ++i) st->P[i] = Pn[i];
     }
+  }
+}
+
+
+// ------------------------------------------------------------------ persistent tracker (G = 1)
+// The whole RO loop of one frame in ONE cooperative launch (all CTAs co-resident): phases are
+// separated by a software grid barrier instead of kernel boundaries, which removes ~3 launches
+// and their tail/latency per iteration.  Phase structure per iteration i:
+//   P1 candidate-pose table (K rows, each CTA a slice)                    | barrier
+//   P2 particle x point evaluation: warp-granular items (4 tiles x 16
+//      particles) handed out by an atomic counter -> no CTA barriers, no
+//      wave tail; warp totals -> global integer atomics                   | barrier
+//   P3 update partials: 256-particle blocks, the same tree as k_update    | barrier
+//   P4 every CTA combines the partials in the same fixed tree (identical
+//      P everywhere), then evaluates E(P) on its slice of the points      | barrier
+//   P5 every CTA sums the centre partials (integers) -> E_c, s-law; CTA 0
+//      writes the trace.
+// Results are bit-identical to the multi-launch path (same helpers, integer sums, same trees).
+constexpr int kItemTiles = 4;     // 8x4 tiles per warp item (= PPT 4 points per lane)
+constexpr int kItemParticles = 16;
+
+struct PArgs {
+  const void* R;
+  const unsigned long long* mask;
+  Geom g;
+  BPArgs bp;
+  Points pts;
+  const float* pst;
+  int K, conv, iters, nblk_upd, ngroups, nchunks;
+  double beta, rho, omega0, v0;
+  const double* T_init;
+  TrackState* st;
+  PartRec* acc;
+  double* E_out;
+  int* n_out;
+  double* trace;
+  double* T_out;
+  double* ptab;
+  int* pflag;
+  double* upart;
+  unsigned long long* cpart;
+  unsigned* work;
+};
+
+// Sense-reversing grid barrier over co-resident CTAs; the gpu-scope fences also invalidate L1
+// (CCTL.IVALL) so data written by other CTAs before the barrier is read fresh after it.
+__device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned arrived = atomicAdd(&st->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      st->bar_count = 0u;
+      __threadfence();
+      atomicExch(&st->bar_gen, gen + 1u);
+    } else {
+      while (*(volatile unsigned*)&st->bar_gen == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  gen += 1u;
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, int flag, unsigned& sum, unsigned& cnt) {
+  const int per = (a.pts.npad + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(a.pts.npad, b0 + per);
+  for (int base = b0; base < b1; base += kThreads) {
+    const int i = base + threadIdx.x;
+    double px[1] = {0.0}, py[1] = {0.0}, pz[1] = {0.0};
+    if (i < b1) { px[0] = __ldcg(a.pts.x + i); py[0] = __ldcg(a.pts.y + i); pz[0] = __ldcg(a.pts.z + i); }
+    double mm[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) mm[q] = m[q];
+    if (flag == 2) eval_points<T, true, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    else if (flag == 1) eval_points<T, false, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
+  }
+}
+
+// CTA total of (sum, cnt) -> thread 0 (fixed-point, like warp_total).
+__device__ __forceinline__ void block_total(unsigned sum, unsigned cnt, unsigned long long* sS, unsigned* sN,
+                                            unsigned long long& S, unsigned& n) {
+  unsigned long long ws;
+  unsigned wn;
+  warp_total(sum, cnt, ws, wn);
+  if ((threadIdx.x & 31) == 0) { sS[threadIdx.x >> 5] = ws; sN[threadIdx.x >> 5] = wn; }
+  __syncthreads();
+  S = 0ull; n = 0u;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) { S += sS[w]; n += sN[w]; }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
+  __shared__ double red[8][256];
+  __shared__ double sP[12], sM[12];
+  __shared__ double sState[4];  // omega, v, Ec, Ebase
+  __shared__ int sFlagC, sNA, sN;
+  __shared__ unsigned sNc;
+  __shared__ unsigned long long sS[kThreads / 32];
+  __shared__ unsigned sNw[kThreads / 32];
+  __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
+  __shared__ int sWFlag[kThreads / 32][kItemParticles];
+  TrackState* st = a.st;
+  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned gen = 0u;
+  if (tid == 0) gen = *(volatile unsigned*)&st->bar_gen;
+  // ---- P0: points (a1/a2), accumulators, pmax
+  {
+    const int stride = gridDim.x * kThreads;
+    double pm = 0.0;
+    for (int i0 = blockIdx.x * kThreads; i0 < a.pts.npad; i0 += stride) {
+      const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
+      const int t = i >> 5, l = i & 31;
+      const int r = (t / a.bp.ntx) * 4 + (l >> 3), c = (t % a.bp.ntx) * 8 + (l & 7);
+      double X = 0.0, Y = 0.0, Z = 0.0;
+      bool valid = false;
+      if (i < a.pts.npad && r < a.bp.nr && c < a.bp.nc) {
+        const int u = c * a.bp.stride, v = r * a.bp.stride;
+        const uint16_t raw = a.bp.depth[(size_t)v * a.bp.W + u];
+        const double d = __dmul_rn((double)raw, a.bp.unit);
+        if (raw != 0 && d < a.bp.max_depth) {
+          valid = true;
+          X = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, a.bp.cx), d), a.bp.fx);
+          Y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, a.bp.cy), d), a.bp.fy);
+          Z = d;
+        }
+      }
+      if (i < a.pts.npad) { a.bp.x[i] = X; a.bp.y[i] = Y; a.bp.z[i] = Z; }
+      pm = fmax(pm, fmax(fabs(X), fmax(fabs(Y), fabs(Z))));
+      const unsigned b = __ballot_sync(0xffffffffu, valid);
+      if (l == 0 && b) atomicAdd(&st->Nvalid, __popc(b));
+    }
+    for (int sft = 16; sft > 0; sft >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, sft));
+    if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
+    for (int k = blockIdx.x * kThreads + tid; k < a.K; k += stride) { a.acc[k].S = 0ull; a.acc[k].n = 0u; }
+  }
+  grid_barrier(st, gen);
+  const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
+  const int N = __ldcg(&st->Nvalid);
+  // ---- initial centre E(T_init)
+  if (tid == 0) {
+    for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
+    sFlagC = explicit_pose(sP, a.g, pmax, sM);
+  }
+  __syncthreads();
+  {
+    unsigned sum = 0u;
+    unsigned cnt = 0u;
+    centre_slice<T>(a, sM, sFlagC, sum, cnt);
+    unsigned long long S;
+    unsigned n;
+    block_total(sum, cnt, sS, sNw, S, n);
+    if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
+  }
+  grid_barrier(st, gen);
+  if (tid == 0) {
+    unsigned long long S = 0ull, n = 0ull;
+    for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
+    sState[0] = a.omega0; sState[1] = a.v0;
+    sState[2] = fitness_of(S, (unsigned)n, a.rho, N);
+    sNc = (unsigned)n;
+    sN = N;
+  }
+  __syncthreads();
+  for (int it = 0; it < a.iters; ++it) {
+    // ---- P1: candidate-pose table
+    for (int k = blockIdx.x * kThreads + tid; k < a.K; k += gridDim.x * kThreads) {
+      double m[12];
+      a.pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
+      double2* row = (double2*)(a.ptab + 12 * (size_t)k);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
+    }
+    grid_barrier(st, gen);
+    // ---- P2: particle x point evaluation, warp-granular dynamic items
+    {
+      const int nitems = a.ngroups * a.nchunks;
+      for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(a.work + it, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= nitems) break;
+        const int group = item / a.nchunks, chunk = item - group * a.nchunks;
+        double px[kItemTiles], py[kItemTiles], pz[kItemTiles];
+#pragma unroll
+        for (int p = 0; p < kItemTiles; ++p) {
+          const int i = (group * kItemTiles + p) * 32 + lane;
+          px[p] = py[p] = pz[p] = 0.0;
+          if (i < a.pts.npad) { px[p] = __ldcg(a.pts.x + i); py[p] = __ldcg(a.pts.y + i); pz[p] = __ldcg(a.pts.z + i); }
+        }
+        const int k0 = chunk * kItemParticles, k1 = min(a.K, k0 + kItemParticles);
+        // stage the item's poses in this warp's shared slot (6 x 16 B per pose, 3 per lane)
+        double2* wp = sWPose[tid >> 5];
+        int* wf = sWFlag[tid >> 5];
+        __syncwarp();
+        for (int q = lane; q < (k1 - k0) * 6; q += 32) wp[q] = __ldcg((const double2*)(a.ptab + 12 * (size_t)k0) + q);
+        if (lane < k1 - k0) wf[lane] = __ldcg(a.pflag + k0 + lane);
+        __syncwarp();
+        for (int k = k0; k < k1; ++k) {
+          const int flag = wf[k - k0];
+          if (flag == 0) continue;  // warp-uniform
+          double m[12];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            const double2 v = wp[(k - k0) * 6 + q];
+            m[2 * q] = v.x;
+            m[2 * q + 1] = v.y;
+          }
+          unsigned sum = 0u;
+          unsigned cnt = 0u;
+          if (flag == 2) eval_points<T, true, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+          else eval_points<T, false, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+          unsigned long long S;
+          unsigned n;
+          warp_total(sum, cnt, S, n);
+          if (lane == 0 && n) {
+            atomicAdd(&a.acc[k].S, S);
+            atomicAdd(&a.acc[k].n, n);
+          }
+        }
+      }
+    }
+    grid_barrier(st, gen);
+    // ---- P3: E_k, advantage set, per-block partials (same tree as k_update)
+    const double Ec = sState[2];
+    for (int b = blockIdx.x; b < a.nblk_upd; b += gridDim.x) {
+      const int k = b * 256 + tid;
+      double q[4] = {0.0, 0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, member = 0.0;
+      if (k < a.K) {
+        const unsigned long long S = __ldcg(&a.acc[k].S);
+        const unsigned n = __ldcg(&a.acc[k].n);
+        const double E = fitness_of(S, n, a.rho, N);
+        a.E_out[k] = E;
+        a.n_out[k] = (int)n;
+        if (E < Ec) {
+          member_delta(a.pst + 6 * (size_t)k, sState[0], sState[1], q, u);
+          member = 1.0;
+        }
+        a.acc[k].S = 0ull;
+        a.acc[k].n = 0u;
+      }
+      red[0][tid] = q[0]; red[1][tid] = q[1]; red[2][tid] = q[2]; red[3][tid] = q[3];
+      red[4][tid] = u[0]; red[5][tid] = u[1]; red[6][tid] = u[2]; red[7][tid] = member;
+      tree8(red, tid);
+      if (tid < 8) a.upart[b * 8 + tid] = red[tid][0];
+      __syncthreads();
+    }
+    grid_barrier(st, gen);
+    // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
+#pragma unroll
+    for (int c = 0; c < 8; ++c) red[c][tid] = 0.0;
+    for (int b = tid; b < a.nblk_upd; b += 256)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) red[c][tid] += __ldcg(a.upart + b * 8 + c);
+    tree8(red, tid);
+    if (tid == 0) {
+      const int nA = (int)red[7][0];
+      sNA = nA;
+      sState[3] = Ec;
+      if (nA > 0) {
+        const double Q[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
+        const double U[3] = {red[4][0], red[5][0], red[6][0]};
+        double Pn[12];
+        apply_mean(Q, U, nA, sP, a.conv, Pn);
+        for (int q = 0; q < 12; ++q) sP[q] = Pn[q];
+        sFlagC = explicit_pose(sP, a.g, pmax, sM);
+      }
+    }
+    __syncthreads();
+    if (sNA > 0) {
+      unsigned sum = 0u;
+      unsigned cnt = 0u;
+      centre_slice<T>(a, sM, sFlagC, sum, cnt);
+      unsigned long long S;
+      unsigned n;
+      block_total(sum, cnt, sS, sNw, S, n);
+      if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
+      grid_barrier(st, gen);  // sNA is identical in every CTA: uniform barrier
+    }
+    // ---- P5: E(P), s-law, trace
+    if (tid == 0) {
+      double Ecn = sState[2];
+      unsigned nc = sNc;
+      if (sNA > 0) {
+        unsigned long long S = 0ull, n = 0ull;
+        for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
+        nc = (unsigned)n;
+        Ecn = fitness_of(S, nc, a.rho, N);
+      }
+      const double om = sState[0], v = sState[1];
+      const double factor = __dadd_rn(a.beta, __dmul_rn(__dsub_rn(1.0, a.beta), Ecn));
+      const double om1 = __dmul_rn(factor, om), v1 = __dmul_rn(factor, v);
+      if (blockIdx.x == 0 && a.trace) {
+        double* r = a.trace + (size_t)it * PFT_TRACE_DOUBLES;
+        const int nA = sNA;
+        r[0] = sState[3]; r[1] = (double)nA; r[2] = om; r[3] = v;
+        for (int q = 0; q < 12; ++q) r[4 + q] = sP[q];
+        r[16] = Ecn; r[17] = om1; r[18] = v1;
+        r[19] = (double)((nA == 0 ? 1 : 0) | (sState[3] == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0));
+        r[20] = (double)nc; r[21] = (double)N; r[22] = 0.0; r[23] = 0.0;
+      }
+      sState[0] = om1; sState[1] = v1; sState[2] = Ecn; sNc = nc;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    for (int q = 0; q < 12; ++q) { a.T_out[q] = sP[q]; st->P[q] = sP[q]; }
+    st->omega = sState[0]; st->v = sState[1]; st->Ec = sState[2]; st->nA = sNA; st->nc = sNc;
+    st->iter = a.iters;
   }
 }
 
@@ -619,6 +968,9 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   if (nranks > 1) { L->acc_full_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kfull, 256); }
   else L->acc_full_off = L->acc_local_off;
   L->part_off = off; off = align_up(off + 8 * sizeof(double) * (size_t)L->nblk_upd, 256);
+  L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
+  L->cpart_off = off; off = align_up(off + 2 * sizeof(unsigned long long) * 148 * 8, 256);
+  L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024, 256);
   L->total = off;
   return PFT_OK;
 }
@@ -673,11 +1025,69 @@ static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin
   }
 }
 
+// Persistent single-launch tracker (G = 1): cooperative launch, all CTAs co-resident.
+template <typename T>
+static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
+                                   const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
+                                   int32_t* n_out, double* trace) {
+  static int grid = 0;
+  if (grid == 0) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kThreads, 0);
+    grid = per_sm * sms;
+    if (grid > 148 * 8) grid = 148 * 8;
+    if (grid < 1) return fail(PFT_ERR_CUDA, "persistent tracker does not fit on the device");
+  }
+  cudaMemsetAsync(c.state(), 0, sizeof(TrackState), c.st);
+  cudaMemsetAsync(c.ws + c.L.work_off, 0, sizeof(unsigned) * (size_t)prm->iters, c.st);
+  Points P = c.pts();
+  PArgs pa;
+  pa.R = c.vol->base + c.vol->L.r_off;
+  pa.mask = (const unsigned long long*)(c.vol->base + c.vol->L.m_off);
+  pa.g = c.vol->g;
+  pa.bp = BPArgs{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height,
+                 prm->stride, c.L.nr, c.L.nc, c.L.ntx, c.L.npad, (double*)P.x, (double*)P.y, (double*)P.z,
+                 &c.state()->Nvalid};
+  pa.pts = P;
+  pa.pst = pst;
+  pa.K = Kp; pa.conv = prm->delta_conv; pa.iters = prm->iters; pa.nblk_upd = c.L.nblk_upd;
+  pa.ngroups = (c.L.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
+  pa.nchunks = (Kp + kItemParticles - 1) / kItemParticles;
+  pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
+  pa.T_init = T_init;
+  pa.st = c.state();
+  pa.acc = (PartRec*)(c.ws + c.L.acc_local_off);
+  pa.E_out = E; pa.n_out = n_out; pa.trace = trace; pa.T_out = T_out;
+  pa.ptab = (double*)(c.ws + c.L.ptab_off);
+  pa.pflag = (int*)(c.ws + c.L.ptab_off + 12 * sizeof(double) * (size_t)Kp);
+  pa.upart = (double*)(c.ws + c.L.part_off);
+  pa.cpart = (unsigned long long*)(c.ws + c.L.cpart_off);
+  pa.work = (unsigned*)(c.ws + c.L.work_off);
+  void* args[] = {&pa};
+  cudaError_t e = cudaSuccess;
+  PFT_LAUNCH(PFT_PROF_TRACK, c.st,
+             e = cudaLaunchCooperativeKernel((const void*)k_track_persistent<T>, dim3(grid), dim3(kThreads), args, 0, c.st));
+  if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "persistent tracker launch: %s", cudaGetErrorString(e));
+  return cuda_check("track (persistent)");
+}
+
+static bool use_persistent() {
+  static const bool on = [] {
+    const char* e = getenv("PFT_TRACK_PERSISTENT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename T>
 static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
                             const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                             int32_t* n_out, double* trace) {
   const int G = c.vol->nranks, r = c.vol->rank;
+  if (G == 1 && use_persistent() && prm->iters <= 1024)
+    return track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
   const int kloc = c.L.kloc;
   const int k_begin = r * kloc;
   const int k_count = max(0, min(Kp, k_begin + kloc) - k_begin);

@@ -1,0 +1,29 @@
+"""Runs pft_track on a seeded config and saves T, E, n, trace (used by tests that compare
+library code paths across processes, e.g. PFT_TRACK_PERSISTENT=0 vs 1)."""
+import sys
+import os
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+
+
+def main(cfg, seed, out):
+    import torch
+    import paper_2509_24236_b200 as pft
+    from synth.configs import config_single, config_tiny, with_desc
+    c = config_tiny(seed=seed) if cfg.startswith("tiny") else config_single(seed=seed)
+    if cfg == "tiny16":
+        c = with_desc(c, storage="f16")
+        c["V"], c["W"] = c["V"].astype(np.float16), c["W"].astype(np.float16)
+    dev = torch.device("cuda", 0)
+    vol = pft.Volume(c["desc"], dev)
+    vol.upload(c["V"], c["W"])
+    r = vol.track(torch.from_numpy(c["depth"]).to(dev), c["intr"], torch.from_numpy(c["T_init"]).to(dev),
+                  torch.from_numpy(c["pst"]).to(dev), c["params"])
+    torch.cuda.synchronize()
+    np.savez(out, **{k: r[k].cpu().numpy() for k in ("T", "E", "n", "trace")})
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3])

@@ -1,5 +1,7 @@
 """GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by element, on
 seeded synthetic inputs (BASELINE.json configs) and the hand-derived golden fixtures."""
+import os
+
 import numpy as np
 import pytest
 
@@ -304,3 +306,20 @@ def test_sequence_track_then_integrate(pft):
         assert np.array_equal(storage_bits(V), storage_bits(ov.V)), f"frame {t}: values differ"
         assert np.array_equal(storage_bits(W), storage_bits(ov.W)), f"frame {t}: weights differ"
     vol.close()
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single"])
+def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
+    """The single-launch persistent tracker (G = 1 default) and the multi-launch path (used for
+    G > 1) share their arithmetic helpers and fixed reduction trees: outputs must be bit-identical."""
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_track.py")
+    outs = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, PFT_TRACK_PERSISTENT=mode)
+        f = str(tmp_path / f"{cfg}_{mode}.npz")
+        subprocess.check_call([sys.executable, helper, cfg, "1", f], env=env)
+        outs[mode] = np.load(f)
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
