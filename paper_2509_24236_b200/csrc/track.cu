@@ -275,6 +275,59 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
   }
 }
 
+// The centre E(P) (a5) drives the search-size law (a8), so its value is reproduced to fp64
+// accuracy: same decisions and loads as eval_points, fp64 lerps, and each |v| rounded to a
+// 2^-44 fixed-point uint64 (exact sums; < 2^63 for N < 2^19 points).
+constexpr double kFixScaleC = 17592186044416.0;   // 2^44
+constexpr double kFixInvC = 1.0 / 17592186044416.0;
+template <typename T, bool FAST, int PPT>
+__device__ __forceinline__ void eval_points_f64(const T* __restrict__ R, const unsigned long long* __restrict__ mask,
+                                                const Geom& g, const double (&m)[12], const double (&px)[PPT],
+                                                const double (&py)[PPT], const double (&pz)[PPT],
+                                                unsigned long long& fix, unsigned& cnt) {
+  uint32_t o[PPT];
+  double fx[PPT], fy[PPT], fz[PPT];
+  bool ok[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const double gx = fma(m[0], px[p], fma(m[1], py[p], fma(m[2], pz[p], m[3])));
+    const double gy = fma(m[4], px[p], fma(m[5], py[p], fma(m[6], pz[p], m[7])));
+    const double gz = fma(m[8], px[p], fma(m[9], py[p], fma(m[10], pz[p], m[11])));
+    float f32;
+    const int ix = cell_split<FAST>(gx, f32), iy = cell_split<FAST>(gy, f32), iz = cell_split<FAST>(gz, f32);
+    fx[p] = gx - floor(gx); fy[p] = gy - floor(gy); fz[p] = gz - floor(gz);
+    ok[p] = pz[p] != 0.0 && (unsigned)ix <= (unsigned)(g.nx - 2) && (unsigned)iy <= (unsigned)(g.ny - 2) &&
+            (unsigned)iz <= (unsigned)(g.nz - 2);
+    o[p] = ok[p] ? offx(ix) + offy(iy, g.sy) + offz(iz, g.sz) : 0u;
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const unsigned long long mw = __ldg(mask + (o[p] >> 6));
+    ok[p] = ok[p] && ((mw >> (o[p] & 63)) & 1ull);
+    float v[8];
+    ld_rec(R + (size_t)(ok[p] ? o[p] : 0u) * 8, v);
+    double w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = (double)v[q];
+    const double c00 = __fma_rn(fx[p], w[1] - w[0], w[0]), c10 = __fma_rn(fx[p], w[3] - w[2], w[2]);
+    const double c01 = __fma_rn(fx[p], w[5] - w[4], w[4]), c11 = __fma_rn(fx[p], w[7] - w[6], w[6]);
+    const double c0 = __fma_rn(fy[p], c10 - c00, c00), c1 = __fma_rn(fy[p], c11 - c01, c01);
+    const double val = __fma_rn(fz[p], c1 - c0, c0);
+    fix += ok[p] ? __double2ull_rn(fabs(val) * kFixScaleC) : 0ull;
+    cnt += ok[p] ? 1u : 0u;
+  }
+}
+
+// Warp total of a 64-bit fixed-point sum and a count (butterfly; same value in every lane).
+__device__ __forceinline__ void warp_total64(unsigned long long fix, unsigned cnt, unsigned long long& S, unsigned& n) {
+  for (int sft = 16; sft > 0; sft >>= 1) {
+    fix += __shfl_xor_sync(0xffffffffu, fix, sft);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, sft);
+  }
+  S = fix;
+  n = cnt;
+}
+
 // Warp total of (fix, cnt) -> 64-bit fixed-point total (same value in every lane).  All lanes must call.
 __device__ __forceinline__ void warp_total(unsigned fix, unsigned cnt, unsigned long long& S, unsigned& n) {
   const unsigned lo = __reduce_add_sync(0xffffffffu, fix & 0xffffu);
@@ -401,6 +454,11 @@ __device__ __forceinline__ double fitness_of(unsigned long long S, unsigned n, d
   if (n > 0u && (double)n >= rho * (double)N) return ((double)S * kFixInv) / (double)n;
   return 1.0;
 }
+// Same for the fp64 centre sums (2^-44 units).
+__device__ __forceinline__ double fitness_c(unsigned long long S, unsigned n, double rho, int N) {
+  if (n > 0u && (double)n >= rho * (double)N) return ((double)S * kFixInvC) / (double)n;
+  return 1.0;
+}
 
 struct TrackArgs {
   TrackState* st;
@@ -499,18 +557,18 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
       for (int i = 0; i < 12; ++i) sm[i] = m[i];
     }
     __syncthreads();
-    unsigned sum = 0u;
+    unsigned long long sum = 0ull;
     unsigned cnt = 0u;
     if (sOk) {
       double m[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) m[i] = sm[i];
-      if (sOk == 2) eval_points<T, true, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
-      else eval_points<T, false, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+      if (sOk == 2) eval_points_f64<T, true, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+      else eval_points_f64<T, false, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
     }
     unsigned long long S;
     unsigned n;
-    warp_total(sum, cnt, S, n);
+    warp_total64(sum, cnt, S, n);
     if ((tid & 31) == 0 && n) {
       atomicAdd(&st->Sc_acc, S);
       atomicAdd(&st->nc_acc, n);
@@ -528,7 +586,7 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
   if (do_eval) {
     const unsigned long long S = vs->Sc_acc;
     nc = vs->nc_acc;
-    Ec = fitness_of(S, nc, a.rho, vs->Nvalid);
+    Ec = fitness_c(S, nc, a.rho, vs->Nvalid);
   }
   st->Sc_acc = 0ull;
   st->nc_acc = 0u;
@@ -693,7 +751,8 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
 }
 
 template <typename T>
-__device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, int flag, unsigned& sum, unsigned& cnt) {
+__device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, int flag, unsigned long long& sum,
+                                             unsigned& cnt) {
   const int per = (a.pts.npad + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(a.pts.npad, b0 + per);
   for (int base = b0; base < b1; base += kThreads) {
@@ -703,17 +762,17 @@ __device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, in
     double mm[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) mm[q] = m[q];
-    if (flag == 2) eval_points<T, true, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
-    else if (flag == 1) eval_points<T, false, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    if (flag == 2) eval_points_f64<T, true, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    else if (flag == 1) eval_points_f64<T, false, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
   }
 }
 
-// CTA total of (sum, cnt) -> thread 0 (fixed-point, like warp_total).
-__device__ __forceinline__ void block_total(unsigned sum, unsigned cnt, unsigned long long* sS, unsigned* sN,
+// CTA total of the centre's (sum, cnt) -> thread 0.
+__device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt, unsigned long long* sS, unsigned* sN,
                                             unsigned long long& S, unsigned& n) {
   unsigned long long ws;
   unsigned wn;
-  warp_total(sum, cnt, ws, wn);
+  warp_total64(sum, cnt, ws, wn);
   if ((threadIdx.x & 31) == 0) { sS[threadIdx.x >> 5] = ws; sN[threadIdx.x >> 5] = wn; }
   __syncthreads();
   S = 0ull; n = 0u;
@@ -777,7 +836,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   }
   __syncthreads();
   {
-    unsigned sum = 0u;
+    unsigned long long sum = 0ull;
     unsigned cnt = 0u;
     centre_slice<T>(a, sM, sFlagC, sum, cnt);
     unsigned long long S;
@@ -790,7 +849,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     unsigned long long S = 0ull, n = 0ull;
     for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
     sState[0] = a.omega0; sState[1] = a.v0;
-    sState[2] = fitness_of(S, (unsigned)n, a.rho, N);
+    sState[2] = fitness_c(S, (unsigned)n, a.rho, N);
     sNc = (unsigned)n;
     sN = N;
   }
@@ -901,7 +960,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     }
     __syncthreads();
     if (sNA > 0) {
-      unsigned sum = 0u;
+      unsigned long long sum = 0ull;
       unsigned cnt = 0u;
       centre_slice<T>(a, sM, sFlagC, sum, cnt);
       unsigned long long S;
@@ -918,7 +977,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         unsigned long long S = 0ull, n = 0ull;
         for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
         nc = (unsigned)n;
-        Ecn = fitness_of(S, nc, a.rho, N);
+        Ecn = fitness_c(S, nc, a.rho, N);
       }
       const double om = sState[0], v = sState[1];
       const double factor = __dadd_rn(a.beta, __dmul_rn(__dsub_rn(1.0, a.beta), Ecn));

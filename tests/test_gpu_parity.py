@@ -11,7 +11,8 @@ from synth.configs import (KINECT_VGA, TrackParams, VolumeDesc, config_single, c
 from synth.rng import Stream
 from synth.scene import Intrinsics, analytic_fill, box_room, perturb, render_depth
 from tests.fixtures import f_track_inputs, golden
-from tests.parity import assert_eval_parity, assert_pose_close, assert_trace_parity, close_E
+from tests.parity import (assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
+                          close_E)
 
 pytestmark = pytest.mark.gpu
 
@@ -184,8 +185,9 @@ def test_track_single(pft, seed):
     r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
     o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
     assert_trace_parity(r["trace"], o["trace"], f"single seed {seed}")
-    np.testing.assert_array_equal(r["n"], o["n"])
-    assert close_E(r["E"], o["E"]).all()
+    ov = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], c["pst"], c["params"], c["T_init"],
+                            f"single seed {seed}")
     assert_pose_close(r["T"], o["T"], "single final")
     vol.close()
 
