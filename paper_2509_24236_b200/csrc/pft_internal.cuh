@@ -30,10 +30,11 @@ __host__ __device__ __forceinline__ uint32_t offx(int x) { return ((uint32_t)(x 
 __host__ __device__ __forceinline__ uint32_t offy(int y, uint32_t sy) { return (uint32_t)(y >> 2) * sy + ((uint32_t)(y & 3) << 2); }
 __host__ __device__ __forceinline__ uint32_t offz(int z, uint32_t sz) { return (uint32_t)(z >> 2) * sz + ((uint32_t)(z & 3) << 4); }
 
-// Cell records: the tracker reads, for trilinear cell (cx,cy,cz), its 8 corner
-// values as ONE 32-byte (fp32) / 16-byte (fp16) record [v000 v100 v010 v110 v001 v101 v011 v111]
-// at record index offx(cx)+offy(cy)+offz(cz) (same brick order as the voxels).  Records are
-// exact copies of the stored values, rebuilt by the fusion step for every touched brick.
+// Cell records: the tracker reads, for trilinear cell (cx,cy,cz), ONE 32-byte
+// (fp32) / 16-byte (fp16) record at record index offx(cx)+offy(cy)+offz(cz) (same brick order as
+// the voxels), rebuilt by the fusion step for every touched brick.  fp32 volumes store the
+// trilinear polynomial coefficients [a b c d e f g h] of the cell (fp64-computed, rounded once);
+// fp16 volumes store the 8 corner values [v000 v100 v010 v110 v001 v101 v011 v111].
 // Beside them, a 1-bit-per-cell in-band mask (bit w of the brick's uint64, w = cell index inside
 // the brick) says whether all 8 corners have |V| < 1 (reading L3); the tracker loads a record
 // only for in-band cells, so its working set is the band, not the search volume.

@@ -266,10 +266,22 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const float c00 = fmaf(fx[p], v[p][1] - v[p][0], v[p][0]), c10 = fmaf(fx[p], v[p][3] - v[p][2], v[p][2]);
-    const float c01 = fmaf(fx[p], v[p][5] - v[p][4], v[p][4]), c11 = fmaf(fx[p], v[p][7] - v[p][6], v[p][6]);
-    const float c0 = fmaf(fy[p], c10 - c00, c00), c1 = fmaf(fy[p], c11 - c01, c01);
-    const float val = fmaf(fz[p], c1 - c0, c0);
+    float val;
+    if (sizeof(T) == 4) {  // polynomial coefficients [a b c d e f g h]
+      const float* k = v[p];
+      const float t1 = fmaf(fz[p], k[7], k[4]);          // e + h fz
+      float t2 = fmaf(fy[p], t1, k[1]);                   // b + fy (e + h fz)
+      t2 = fmaf(fz[p], k[5], t2);                         //   + f fz
+      const float t3 = fmaf(fz[p], k[6], k[2]);           // c + g fz
+      float acc = fmaf(fz[p], k[3], k[0]);                // a + d fz
+      acc = fmaf(fy[p], t3, acc);
+      val = fmaf(fx[p], t2, acc);
+    } else {               // corner values
+      const float c00 = fmaf(fx[p], v[p][1] - v[p][0], v[p][0]), c10 = fmaf(fx[p], v[p][3] - v[p][2], v[p][2]);
+      const float c01 = fmaf(fx[p], v[p][5] - v[p][4], v[p][4]), c11 = fmaf(fx[p], v[p][7] - v[p][6], v[p][6]);
+      const float c0 = fmaf(fy[p], c10 - c00, c00), c1 = fmaf(fy[p], c11 - c01, c01);
+      val = fmaf(fz[p], c1 - c0, c0);
+    }
     fix += ok[p] ? __float2uint_rn(fabsf(val) * (float)kFixScale) : 0u;
     cnt += ok[p] ? 1u : 0u;
   }
@@ -280,8 +292,11 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
 // 2^-44 fixed-point uint64 (exact sums; < 2^63 for N < 2^19 points).
 constexpr double kFixScaleC = 17592186044416.0;   // 2^44
 constexpr double kFixInvC = 1.0 / 17592186044416.0;
+template <typename T> __device__ __forceinline__ float ldv(const T* p);
+template <> __device__ __forceinline__ float ldv<float>(const float* p) { return __ldg(p); }
+template <> __device__ __forceinline__ float ldv<__half>(const __half* p) { return __half2float(__ldg(p)); }
 template <typename T, bool FAST, int PPT>
-__device__ __forceinline__ void eval_points_f64(const T* __restrict__ R, const unsigned long long* __restrict__ mask,
+__device__ __forceinline__ void eval_points_f64(const T* __restrict__ V, const unsigned long long* __restrict__ mask,
                                                 const Geom& g, const double (&m)[12], const double (&px)[PPT],
                                                 const double (&py)[PPT], const double (&pz)[PPT],
                                                 unsigned long long& fix, unsigned& cnt) {
@@ -304,11 +319,16 @@ __device__ __forceinline__ void eval_points_f64(const T* __restrict__ R, const u
   for (int p = 0; p < PPT; ++p) {
     const unsigned long long mw = __ldg(mask + (o[p] >> 6));
     ok[p] = ok[p] && ((mw >> (o[p] & 63)) & 1ull);
-    float v[8];
-    ld_rec(R + (size_t)(ok[p] ? o[p] : 0u) * 8, v);
+    // exact stored corner values (brick order), not the record
+    const uint32_t b = ok[p] ? o[p] : 0u;
+    const uint32_t dx = ((b & 3u) == 3u) ? 64u - 3u : 1u;              // x + 1 crosses into the next brick?
+    const uint32_t dy = (((b >> 2) & 3u) == 3u) ? g.sy - 12u : 4u;
+    const uint32_t dz = (((b >> 4) & 3u) == 3u) ? g.sz - 48u : 16u;
     double w[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w[q] = (double)v[q];
+    w[0] = ldv(V + b);           w[1] = ldv(V + b + dx);
+    w[2] = ldv(V + b + dy);      w[3] = ldv(V + b + dx + dy);
+    w[4] = ldv(V + b + dz);      w[5] = ldv(V + b + dx + dz);
+    w[6] = ldv(V + b + dy + dz); w[7] = ldv(V + b + dx + dy + dz);
     const double c00 = __fma_rn(fx[p], w[1] - w[0], w[0]), c10 = __fma_rn(fx[p], w[3] - w[2], w[2]);
     const double c01 = __fma_rn(fx[p], w[5] - w[4], w[4]), c11 = __fma_rn(fx[p], w[7] - w[6], w[6]);
     const double c0 = __fma_rn(fy[p], c10 - c00, c00), c1 = __fma_rn(fy[p], c11 - c01, c01);
@@ -521,7 +541,7 @@ __global__ void k_backproject(BPArgs a) {
 
 // a5 + a8: E(P) of the current pose; the last CTA closes the iteration (s-law, trace).
 struct CentreArgs {
-  const void* R;
+  const void* V;                    // stored values (the centre lerps exact corner values in fp64)
   const unsigned long long* mask;
   Geom g;
   Points pts;
@@ -563,8 +583,8 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
       double m[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) m[i] = sm[i];
-      if (sOk == 2) eval_points_f64<T, true, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
-      else eval_points_f64<T, false, kCentrePPT>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+      if (sOk == 2) eval_points_f64<T, true, kCentrePPT>((const T*)a.V, a.mask, a.g, m, px, py, pz, sum, cnt);
+      else eval_points_f64<T, false, kCentrePPT>((const T*)a.V, a.mask, a.g, m, px, py, pz, sum, cnt);
     }
     unsigned long long S;
     unsigned n;
@@ -709,6 +729,7 @@ constexpr int kItemParticles = 16;
 
 struct PArgs {
   const void* R;
+  const void* V;
   const unsigned long long* mask;
   Geom g;
   BPArgs bp;
@@ -762,8 +783,8 @@ __device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, in
     double mm[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) mm[q] = m[q];
-    if (flag == 2) eval_points_f64<T, true, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
-    else if (flag == 1) eval_points_f64<T, false, 1>((const T*)a.R, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    if (flag == 2) eval_points_f64<T, true, 1>((const T*)a.V, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    else if (flag == 1) eval_points_f64<T, false, 1>((const T*)a.V, a.mask, a.g, mm, px, py, pz, sum, cnt);
   }
 }
 
@@ -1061,7 +1082,7 @@ static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_in
 
 template <typename T>
 static void launch_centre(const Launch& c, int initial, double beta, double rho, double* trace, double* T_out) {
-  CentreArgs ca{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
+  CentreArgs ca{c.vol->base + c.vol->L.v_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
   int grid = (c.L.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
   PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
 }
@@ -1104,6 +1125,7 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   Points P = c.pts();
   PArgs pa;
   pa.R = c.vol->base + c.vol->L.r_off;
+  pa.V = c.vol->base + c.vol->L.v_off;
   pa.mask = (const unsigned long long*)(c.vol->base + c.vol->L.m_off);
   pa.g = c.vol->g;
   pa.bp = BPArgs{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height,

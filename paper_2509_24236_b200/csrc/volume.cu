@@ -91,9 +91,19 @@ __device__ __forceinline__ bool build_record(const Geom& g, const T* __restrict_
             V[x0 + y0 + z1], V[x1 + y0 + z1], V[x0 + y1 + z1], V[x1 + y1 + z1]};
   T* dst = R + (size_t)(x0 + y0 + z0) * 8;
   if (sizeof(T) == 4) {
+    // fp32 volumes: trilinear polynomial coefficients, computed in fp64 and rounded once:
+    // v(f) = a + b fx + c fy + d fz + e fx fy + f fx fz + g fy fz + h fx fy fz
+    double w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = (double)*(const float*)&r[i];
+    const double ca = w[0], cb = w[1] - w[0], cc = w[2] - w[0], cd = w[4] - w[0];
+    const double ce = (w[3] - w[2]) - (w[1] - w[0]);
+    const double cf = (w[5] - w[4]) - (w[1] - w[0]);
+    const double cg = (w[6] - w[4]) - (w[2] - w[0]);
+    const double ch = ((w[7] - w[6]) - (w[5] - w[4])) - ((w[3] - w[2]) - (w[1] - w[0]));
     float4* d = (float4*)dst;
-    d[0] = make_float4(*(float*)&r[0], *(float*)&r[1], *(float*)&r[2], *(float*)&r[3]);
-    d[1] = make_float4(*(float*)&r[4], *(float*)&r[5], *(float*)&r[6], *(float*)&r[7]);
+    d[0] = make_float4((float)ca, (float)cb, (float)cc, (float)cd);
+    d[1] = make_float4((float)ce, (float)cf, (float)cg, (float)ch);
   } else {
     uint4 u;
     u.x = (uint32_t)*(unsigned short*)&r[0] | ((uint32_t)*(unsigned short*)&r[1] << 16);
