@@ -185,12 +185,8 @@ __device__ __forceinline__ void ld_rec(const float* p, float (&v)[8]) {
       : "l"(p));
 }
 __device__ __forceinline__ void ld_rec(const __half* p, float (&v)[8]) {
-  // Two 64-bit loads: the single 128-bit form (ld.global[.nc].v4.b32) raised "misaligned address"
-  // in the <__half, 4> specialisation on B200 although the address is base + 16*o with a
-  // 4 KB-aligned base (cuda-gdb errorpc on the LDG.E.128; A/B in DESIGN.md §9).
   unsigned u0, u1, u2, u3;
-  asm("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(u0), "=r"(u1) : "l"(p));
-  asm("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(u2), "=r"(u3) : "l"(p + 4));
+  asm("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3) : "l"(p));
   const unsigned u[4] = {u0, u1, u2, u3};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -241,7 +237,8 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
     const int ix = cell_split<FAST>(gx, fx[p]), iy = cell_split<FAST>(gy, fy[p]), iz = cell_split<FAST>(gz, fz[p]);
     ok[p] = pz[p] != 0.0 && (unsigned)ix <= (unsigned)(g.nx - 2) && (unsigned)iy <= (unsigned)(g.ny - 2) &&
             (unsigned)iz <= (unsigned)(g.nz - 2);
-    o[p] = ok[p] ? offx(ix) + offy(iy, g.sy) + offz(iz, g.sz) : 0u;
+    // computed unconditionally and masked (no branch): out-of-range lanes use cell 0
+    o[p] = (offx(ix) + offy(iy, g.sy) + offz(iz, g.sz)) & (0u - (uint32_t)ok[p]);
   }
   // in band iff all 8 corners |V| < 1 (reading L3): one bit per cell, precomputed from the
   // same stored values by the record builder
@@ -256,13 +253,20 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
     }
   }
 #endif
+  // Addresses are formed as byte offsets from integer-selected indices (one IMAD.WIDE each):
+  // the predicated "CS2R; @!P IMAD.WIDE; IADD3 r,UR,r" idiom ptxas 12.9 emitted for
+  // base + (ok ? o : 0) * size read a stale register on B200.
+  const char* mbase = reinterpret_cast<const char*>(mask);
+  const char* rbase = reinterpret_cast<const char*>(R);
 #pragma unroll
-  for (int p = 0; p < PPT; ++p) mw[p] = __ldg(mask + (o[p] >> 6));
+  for (int p = 0; p < PPT; ++p)
+    mw[p] = __ldg(reinterpret_cast<const unsigned long long*>(mbase + (size_t)(o[p] >> 6) * 8u));
   float v[PPT][8];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     ok[p] = ok[p] && ((mw[p] >> (o[p] & 63)) & 1ull);
-    ld_rec(R + (size_t)(ok[p] ? o[p] : 0u) * 8, v[p]);
+    const uint32_t orec = o[p] & (0u - (uint32_t)ok[p]);
+    ld_rec(reinterpret_cast<const T*>(rbase + (size_t)orec * (8u * sizeof(T))), v[p]);
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
@@ -804,7 +808,11 @@ __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt
 
 template <typename T>
 __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
-  __shared__ double red[8][256];
+  // red (update phases) and sPart (evaluation phase) are never live at the same time
+  constexpr size_t kRedBytes = 8 * 256 * sizeof(double);
+  constexpr size_t kPartBytes = (kThreads / 32) * kItemParticles * 33 * sizeof(unsigned long long);
+  __shared__ __align__(16) unsigned char sUnion[kRedBytes > kPartBytes ? kRedBytes : kPartBytes];
+  double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
   __shared__ int sFlagC, sNA, sN;
@@ -813,6 +821,9 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   __shared__ unsigned sNw[kThreads / 32];
   __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
   __shared__ int sWFlag[kThreads / 32][kItemParticles];
+  // per-lane partials of the item's particles: (fix | cnt << 32), rows padded against bank conflicts
+  unsigned long long (*sPart)[kItemParticles][33] =
+      reinterpret_cast<unsigned long long (*)[kItemParticles][33]>(sUnion);
   TrackState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned gen = 0u;
@@ -909,28 +920,40 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         for (int q = lane; q < (k1 - k0) * 6; q += 32) wp[q] = __ldcg((const double2*)(a.ptab + 12 * (size_t)k0) + q);
         if (lane < k1 - k0) wf[lane] = __ldcg(a.pflag + k0 + lane);
         __syncwarp();
+        unsigned long long (*part)[33] = sPart[tid >> 5];
         for (int k = k0; k < k1; ++k) {
           const int flag = wf[k - k0];
-          if (flag == 0) continue;  // warp-uniform
-          double m[12];
-#pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            const double2 v = wp[(k - k0) * 6 + q];
-            m[2 * q] = v.x;
-            m[2 * q + 1] = v.y;
-          }
           unsigned sum = 0u;
           unsigned cnt = 0u;
-          if (flag == 2) eval_points<T, true, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
-          else eval_points<T, false, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
-          unsigned long long S;
-          unsigned n;
-          warp_total(sum, cnt, S, n);
-          if (lane == 0 && n) {
-            atomicAdd(&a.acc[k].S, S);
-            atomicAdd(&a.acc[k].n, n);
+          if (flag != 0) {  // warp-uniform
+            double m[12];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              const double2 v = wp[(k - k0) * 6 + q];
+              m[2 * q] = v.x;
+              m[2 * q + 1] = v.y;
+            }
+            if (flag == 2) eval_points<T, true, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+            else eval_points<T, false, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+          }
+          part[k - k0][lane] = (unsigned long long)sum | ((unsigned long long)cnt << 32);
+        }
+        __syncwarp();
+        // lane j < #particles reduces particle j's row (exact integers) and issues its atomics
+        if (lane < k1 - k0) {
+          unsigned long long S = 0ull;
+          unsigned n = 0u;
+          for (int l = 0; l < 32; ++l) {
+            const unsigned long long w = part[lane][l];
+            S += w & 0xffffffffull;
+            n += (unsigned)(w >> 32);
+          }
+          if (n) {
+            atomicAdd(&a.acc[k0 + lane].S, S);
+            atomicAdd(&a.acc[k0 + lane].n, n);
           }
         }
+        __syncwarp();
       }
     }
     grid_barrier(st, gen);
