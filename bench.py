@@ -52,6 +52,9 @@ def make_workload(args, n_steps, world):
     from synth.scene import Intrinsics  # noqa: F401
     nf = args.map_frames + n_steps
     seq = Sequence("Q", seed=args.seed, n_frames=max(nf, 48), K=K_PER_GPU * world, iters=ITERS)
+    if os.environ.get("PFT_BENCH_PST_ORDER"):
+        from synth.configs import make_pst
+        seq.pst = make_pst(args.seed, seq.K, os.environ["PFT_BENCH_PST_ORDER"])
     map_depth = [seq.depth(t) for t in range(args.map_frames)]
     steps = []
     for i in range(n_steps):

@@ -739,7 +739,7 @@ struct PArgs {
   BPArgs bp;
   Points pts;
   const float* pst;
-  int K, conv, iters, nblk_upd, ngroups, nchunks;
+  int K, conv, iters, nblk_upd, ngroups, nchunks, sched;
   double beta, rho, omega0, v0;
   const double* T_init;
   TrackState* st;
@@ -815,7 +815,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
-  __shared__ int sFlagC, sNA, sN;
+  __shared__ int sFlagC, sNA, sN, sItem;
   __shared__ unsigned sNc;
   __shared__ unsigned long long sS[kThreads / 32];
   __shared__ unsigned sNw[kThreads / 32];
@@ -896,14 +896,20 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
     }
     grid_barrier(st, gen);
-    // ---- P2: particle x point evaluation, warp-granular dynamic items
+    // ---- P2: particle x point evaluation, warp-granular items (group-major: item = group * nchunks
+    // + chunk).  sched 0: one global dynamic queue; sched 1: CTA c owns the contiguous range
+    // [c*n/G, (c+1)*n/G) (its warps share one image region -> L1 reuse), handed out by a CTA counter.
     {
       const int nitems = a.ngroups * a.nchunks;
+      const int r0 = (int)((long long)nitems * blockIdx.x / gridDim.x);
+      const int r1 = (int)((long long)nitems * (blockIdx.x + 1) / gridDim.x);
+      if (tid == 0) sItem = 0;
+      __syncthreads();
       for (;;) {
         int item = 0;
-        if (lane == 0) item = (int)atomicAdd(a.work + it, 1u);
+        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(a.work + it, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= nitems) break;
+        if (item >= (a.sched == 1 ? r1 : nitems)) break;
         const int group = item / a.nchunks, chunk = item - group * a.nchunks;
         double px[kItemTiles], py[kItemTiles], pz[kItemTiles];
 #pragma unroll
@@ -1159,6 +1165,8 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.K = Kp; pa.conv = prm->delta_conv; pa.iters = prm->iters; pa.nblk_upd = c.L.nblk_upd;
   pa.ngroups = (c.L.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
   pa.nchunks = (Kp + kItemParticles - 1) / kItemParticles;
+  static const int sched = [] { const char* e = getenv("PFT_EVAL_SCHED"); return e ? atoi(e) : 0; }();
+  pa.sched = sched;
   pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
   pa.T_init = T_init;
   pa.st = c.state();

@@ -43,9 +43,20 @@ KINECT_VGA = Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)
 TINY_CAM = Intrinsics(131.25, 131.25, 39.5, 29.5, 80, 60)
 
 
-def make_pst(seed: int, K: int) -> np.ndarray:
-    """Particle-swarm template: K x 6 uniform in [-1,1], rounded to fp32 (stream 3)."""
-    return Stream(seed, 3).symmetric(6 * K).astype(np.float32).reshape(K, 6)
+def make_pst(seed: int, K: int, order: str = "none") -> np.ndarray:
+    """Particle-swarm template: K x 6 uniform in [-1,1], rounded to fp32 (stream 3).
+    order="morton" returns the same set of rows sorted along a 6-D Morton curve (10 bits per
+    axis), so neighbouring rows are similar delta poses (an input layout choice: the sample set,
+    and hence the method, is unchanged)."""
+    pst = Stream(seed, 3).symmetric(6 * K).astype(np.float32).reshape(K, 6)
+    if order == "morton":
+        q = np.clip(((pst.astype(np.float64) + 1.0) * 512.0).astype(np.int64), 0, 1023)
+        key = np.zeros(K, dtype=np.int64)
+        for bit in range(9, -1, -1):
+            for ax in range(6):
+                key = (key << 1) | ((q[:, ax] >> bit) & 1)
+        pst = pst[np.argsort(key, kind="stable")]
+    return pst
 
 
 def init_noise(seed: int, t: int, T_gt, deg, cm):
