@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pft_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-TRACE_DOUBLES = 20
+TRACE_DOUBLES = 24
 
 
 def build(force=False):
@@ -43,7 +43,10 @@ class Intrinsics(C.Structure):
 class TrackParams(C.Structure):
     _fields_ = [("omega0_deg", C.c_double), ("v0_cm", C.c_double), ("beta", C.c_double),
                 ("iters", C.c_int32), ("stride", C.c_int32), ("min_inband_frac", C.c_double),
-                ("delta_conv", C.c_int32), ("update_rule", C.c_int32), ("topk", C.c_int32)]
+                ("delta_conv", C.c_int32), ("update_rule", C.c_int32), ("topk", C.c_int32),
+                ("nsched", C.c_int32), ("sched_K", C.c_int32 * 4), ("sched_sx", C.c_int32 * 4),
+                ("sched_sy", C.c_int32 * 4), ("min_search_deg", C.c_double), ("min_search_cm", C.c_double),
+                ("guard", C.c_int32), ("stall_limit", C.c_int32)]
 
 
 _lib = None
@@ -56,6 +59,8 @@ def lib():
         P = C.c_void_p
         _lib.ora_backproject.restype = C.c_int32
         _lib.ora_backproject.argtypes = [P, P, C.c_int32, C.c_double, P]
+        _lib.ora_backproject2.restype = C.c_int32
+        _lib.ora_backproject2.argtypes = [P, P, C.c_int32, C.c_int32, C.c_double, P]
         _lib.ora_query.restype = C.c_int32
         _lib.ora_query.argtypes = [P, P, P, P, P]
         _lib.ora_fitness.restype = C.c_double
@@ -99,8 +104,21 @@ def make_intr(k):
 
 
 def make_params(p):
+    def arr(name):
+        v = list(getattr(p, name, (0, 0, 0, 0))) + [0, 0, 0, 0]
+        return (C.c_int32 * 4)(*v[:4])
     return TrackParams(p.omega0_deg, p.v0_cm, p.beta, p.iters, p.stride, p.min_inband_frac,
-                       p.delta_conv, p.update_rule, p.topk)
+                       p.delta_conv, p.update_rule, p.topk, getattr(p, "nsched", 0), arr("sched_K"), arr("sched_sx"),
+                       arr("sched_sy"), getattr(p, "min_search_deg", 0.0), getattr(p, "min_search_cm", 0.0),
+                       getattr(p, "guard", 0), getattr(p, "stall_limit", 0))
+
+
+def densest_slots(intr, params):
+    """Point slots of the densest point set a run uses (workspace size)."""
+    sets = [(params.stride, params.stride)]
+    for j in range(getattr(params, "nsched", 0)):
+        sets.append((params.sched_sx[j], params.sched_sy[j]))
+    return max((-(-intr.height // sy)) * (-(-intr.width // sx)) for sx, sy in sets)
 
 
 def storage_dtype(desc):
@@ -163,8 +181,7 @@ class OracleVolume:
         T_init = np.ascontiguousarray(T_init, dtype=np.float64)
         pst = np.ascontiguousarray(pst, dtype=np.float32)
         K = pst.shape[0]
-        s = params.stride
-        ws = np.zeros(3 * (-(-intr.height // s)) * (-(-intr.width // s)))
+        ws = np.zeros(3 * densest_slots(intr, params))
         T = np.zeros(12)
         E = np.zeros(K)
         n = np.zeros(K, dtype=np.int32)
@@ -190,11 +207,13 @@ class OracleVolume:
         return dict(E=E, n=n, N=N, margin=mg)
 
 
-def backproject(depth, intr, stride, max_depth_m=8.0):
+def backproject(depth, intr, stride, max_depth_m=8.0, stride_y=None):
+    """O2 strided points; stride_y given: 2-D strides (stride on columns, stride_y on rows)."""
     depth = np.ascontiguousarray(depth, dtype=np.uint16)
-    ws = np.zeros(3 * (-(-intr.height // stride)) * (-(-intr.width // stride)))
+    sy = stride if stride_y is None else stride_y
+    ws = np.zeros(3 * (-(-intr.height // sy)) * (-(-intr.width // stride)))
     ci = make_intr(intr)
-    N = lib().ora_backproject(_p(depth), C.byref(ci), stride, max_depth_m, _p(ws))
+    N = lib().ora_backproject2(_p(depth), C.byref(ci), stride, sy, max_depth_m, _p(ws))
     return ws[: 3 * N].reshape(N, 3)
 
 

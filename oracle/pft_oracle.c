@@ -51,11 +51,21 @@ typedef struct {
   int32_t iters, stride;
   double min_inband_frac;
   int32_t delta_conv;  /* 0 camera-centred (L10 default), 1 world-literal */
-  int32_t update_rule; /* 0 plain mean (paper, L14) */
+  int32_t update_rule; /* 0 plain mean (paper, L14); 1 weighted by E_base - E_k (NEXT F3) */
   int32_t topk;
+  /* NEXT F1, the paper's schedule: iteration i uses the first sched_K[i % nsched]
+   * template rows and the point set of strides (sched_sx, sched_sy); nsched = 0: (all, stride). */
+  int32_t nsched;
+  int32_t sched_K[4], sched_sx[4], sched_sy[4];
+  /* F1 convergence stop: stop after an iteration whose new s has omega < min_search_deg
+   * and v < min_search_cm (both 0: off). */
+  double min_search_deg, min_search_cm;
+  /* NEXT F3: guard = keep P^(i-1) when E(P^(i)) > E_base (a stall);
+   * stall_limit > 0: stop after that many consecutive iterations without a pose change. */
+  int32_t guard, stall_limit;
 } ora_track_params;
 
-#define ORA_TRACE_DOUBLES 20
+#define ORA_TRACE_DOUBLES 24
 
 /* ------------------------------------------------------------------ storage */
 /* Stored value -> fp64 (exact for both storage precisions). */
@@ -87,11 +97,11 @@ double ora_round_to_storage(double x, int32_t storage) {
  * O2 strided back-projection (L20): pixels (u,v) = (stride*c, stride*r),
  * row-major over r < ceil(H/stride), c < ceil(W/stride); p = ((u-cx)d/fx, (v-cy)d/fy, d).
  * Writes up to ceil(H/s)*ceil(W/s) points (x,y,z interleaved); returns N. */
-int32_t ora_backproject(const uint16_t *depth, const ora_intrinsics *K, int32_t stride,
-                        double max_depth_m, double *pts) {
+int32_t ora_backproject2(const uint16_t *depth, const ora_intrinsics *K, int32_t sx, int32_t sy,
+                         double max_depth_m, double *pts) {
   int32_t n = 0;
-  for (int32_t v = 0; v < K->height; v += stride) {
-    for (int32_t u = 0; u < K->width; u += stride) {
+  for (int32_t v = 0; v < K->height; v += sy) {
+    for (int32_t u = 0; u < K->width; u += sx) {
       uint16_t raw = depth[(size_t)v * K->width + u];
       double d = (double)raw * K->depth_unit_m;
       if (raw == 0 || !(d < max_depth_m)) continue;
@@ -102,6 +112,12 @@ int32_t ora_backproject(const uint16_t *depth, const ora_intrinsics *K, int32_t 
     }
   }
   return n;
+}
+
+/* Same with one stride on both axes (the configs' 4x4 = 1/16 rate, L20). */
+int32_t ora_backproject(const uint16_t *depth, const ora_intrinsics *K, int32_t stride,
+                        double max_depth_m, double *pts) {
+  return ora_backproject2(depth, K, stride, stride, max_depth_m, pts);
 }
 
 /* ------------------------------------------------------------------ O3 */
@@ -246,38 +262,57 @@ void ora_apply_delta(const double dR[9], const double u[3], const double P[12], 
 
 /* ------------------------------------------------------------------ O7 / O8 */
 /* Randomized optimization, PAPER.md:192-208 step by step (O7):
- *   P = T_init; s = (omega0, v0); E_c = E(P).
+ *   P = T_init; s = (omega0, v0).
  *   for i = 1..iters:
- *     for every k: dP_k from template row k scaled by s (L8); E_k = E(dP_k P)   (eq. E)
- *     A = {k : E_k < E_c}
- *     if A nonempty: q = sum_{k in A, ascending} q_k / |.|, u = mean_A u_k
- *                    P = avg-delta * P (O6 convention); E_c = E(P)
- *     s = (beta + (1-beta) E_c) s                                                 (PAPER.md:207, L17)
- *   Outputs: P, last iteration's E_k / n_k, per-iteration trace (O8).
- * Returns N (number of back-projected points); 0 means EMPTY_CLOUD (P = T_init, E = 1, n = 0).
- * pts_ws must hold ceil(H/stride)*ceil(W/stride)*3 doubles.  nthreads > 1 splits the
- * independent particle evaluations across OpenMP threads (arithmetic unchanged). */
+ *     iteration's particles K_i and point set X_i (F1 schedule, else all rows and the stride);
+ *     E_base = E(P) on X_i (L11: recomputed when X_i changes, else the E_c of the last iteration)
+ *     for every k < K_i: dP_k from template row k scaled by s (L8); E_k = E(dP_k P)  (eq. E)
+ *     A = {k : E_k < E_base}
+ *     if A nonempty: q = sum_{k in A, ascending} w_k q_k / |.|, u = sum w_k u_k / sum w_k
+ *                    (w_k = 1: the paper's mean, L13/L14; w_k = E_base - E_k: F3 weighted)
+ *                    P' = avg-delta * P (O6 convention); E_c = E(P') on X_i
+ *                    F3 guard: if E_c > E_base keep P (a stall)
+ *     else E_c = E_base (P unchanged, a stall)
+ *     s = (beta + (1-beta) E_c) s                                             (PAPER.md:207, L17)
+ *     F1/F3 stop: s below min_search, or stall_limit consecutive stalls
+ *   Outputs: P, the last executed iteration's E_k / n_k (rows >= K_i: E = 1, n = 0), trace (O8).
+ * Trace row (24 doubles): E_base, |A|, omega_i, v_i, P(12), E_c, omega', v', flags (bit0 A empty,
+ * bit1 E_base == 1, bit2 no valid point, bit3 guard rejected, bit4 stopped here, bit5 not run),
+ * n_c, N_i, K_i, sx + 1000 sy.
+ * Returns N of the first iteration's point set (0: EMPTY_CLOUD semantics: P = T_init, E = 1, n = 0).
+ * pts_ws must hold ceil(H/sy)*ceil(W/sx)*3 doubles for the densest point set used.  nthreads > 1
+ * splits the independent particle evaluations across OpenMP threads (arithmetic unchanged). */
 int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth,
                   const ora_intrinsics *Kin, const double T_init[12], const float *pst, int32_t K,
                   const ora_track_params *prm, double *pts_ws, double T_out[12], double *E_out,
                   int32_t *n_out, double *trace, double *min_margin, int32_t nthreads) {
-  int32_t N = ora_backproject(depth, Kin, prm->stride, D->max_depth_m, pts_ws);
-  memcpy(T_out, T_init, 12 * sizeof(double));
-  if (N == 0) {
-    for (int32_t k = 0; k < K; ++k) { E_out[k] = 1.0; n_out[k] = 0; }
-    return 0;
-  }
   double P[12];
   memcpy(P, T_init, sizeof P);
   double omega = prm->omega0_deg, v = prm->v0_cm;
-  int32_t nc;
-  double Ec = ora_fitness(V, D, pts_ws, N, P, prm->min_inband_frac, &nc, min_margin);
   double *q_all = (double *)malloc(sizeof(double) * 4 * (size_t)K);
   double *u_all = (double *)malloc(sizeof(double) * 3 * (size_t)K);
-  for (int32_t it = 0; it < prm->iters; ++it) {
+  int32_t cur_sx = -1, cur_sy = -1, N = 0, N_first = -1, nc = 0, stalls = 0, it;
+  double Ec = 1.0;
+  for (int32_t k = 0; k < K; ++k) { E_out[k] = 1.0; n_out[k] = 0; }
+  for (it = 0; it < prm->iters; ++it) {
+    int32_t Ki = K, sx = prm->stride, sy = prm->stride;
+    if (prm->nsched > 0) {
+      int32_t j = it % prm->nsched;
+      Ki = prm->sched_K[j] < K ? prm->sched_K[j] : K;
+      sx = prm->sched_sx[j];
+      sy = prm->sched_sy[j];
+    }
+    double Ebase = Ec;
+    if (sx != cur_sx || sy != cur_sy) {  /* X_i changed (always at i = 1): recompute the baseline */
+      N = ora_backproject2(depth, Kin, sx, sy, D->max_depth_m, pts_ws);
+      cur_sx = sx;
+      cur_sy = sy;
+      Ebase = ora_fitness(V, D, pts_ws, N, P, prm->min_inband_frac, &nc, min_margin);
+    }
+    if (N_first < 0) N_first = N;
     double margin = 1.0;
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 4) reduction(min : margin)
-    for (int32_t k = 0; k < K; ++k) {
+    for (int32_t k = 0; k < Ki; ++k) {
       double dR[9], Tk[12];
       ora_delta(pst + 6 * (size_t)k, omega, v, dR, q_all + 4 * (size_t)k, u_all + 3 * (size_t)k);
       ora_apply_delta(dR, u_all + 3 * (size_t)k, P, prm->delta_conv, Tk);
@@ -285,43 +320,66 @@ int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth
       E_out[k] = ora_fitness(V, D, pts_ws, N, Tk, prm->min_inband_frac, &n_out[k], &mk);
       if (mk < margin) margin = mk;
     }
+    for (int32_t k = Ki; k < K; ++k) { E_out[k] = 1.0; n_out[k] = 0; }
     if (min_margin && margin < *min_margin) *min_margin = margin;
-    double Ebase = Ec;
-    double Q[4] = {0, 0, 0, 0}, U[3] = {0, 0, 0};
+    double Q[4] = {0, 0, 0, 0}, U[3] = {0, 0, 0}, Wsum = 0.0;
     int32_t nA = 0;
-    for (int32_t k = 0; k < K; ++k) {
+    for (int32_t k = 0; k < Ki; ++k) {
       if (E_out[k] < Ebase) {
-        for (int j = 0; j < 4; ++j) Q[j] += q_all[4 * (size_t)k + j];
-        for (int j = 0; j < 3; ++j) U[j] += u_all[3 * (size_t)k + j];
+        double w = prm->update_rule == 1 ? Ebase - E_out[k] : 1.0;
+        for (int j = 0; j < 4; ++j) Q[j] += w * q_all[4 * (size_t)k + j];
+        for (int j = 0; j < 3; ++j) U[j] += w * u_all[3 * (size_t)k + j];
+        Wsum += w;
         nA++;
       }
     }
+    int32_t rejected = 0, ncn = nc;
+    Ec = Ebase;
     if (nA > 0) {
       double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
       double qbar[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
-      double ubar[3] = {U[0] / nA, U[1] / nA, U[2] / nA};
+      double ubar[3] = {U[0] / Wsum, U[1] / Wsum, U[2] / Wsum};
       double Rbar[9], Pn[12];
       ora_quat_to_R(qbar, Rbar);
       ora_apply_delta(Rbar, ubar, P, prm->delta_conv, Pn);
-      memcpy(P, Pn, sizeof P);
-      Ec = ora_fitness(V, D, pts_ws, N, P, prm->min_inband_frac, &nc, min_margin);
+      double En = ora_fitness(V, D, pts_ws, N, Pn, prm->min_inband_frac, &ncn, min_margin);
+      if (prm->guard && En > Ebase) {
+        rejected = 1;
+      } else {
+        memcpy(P, Pn, sizeof P);
+        Ec = En;
+        nc = ncn;
+      }
     }
+    stalls = (nA == 0 || rejected) ? stalls + 1 : 0;
     double om_i = omega, v_i = v;
     double factor = prm->beta + (1.0 - prm->beta) * Ec;
     omega = factor * omega;
     v = factor * v;
+    int32_t stop = ((prm->min_search_deg > 0.0 || prm->min_search_cm > 0.0) && omega < prm->min_search_deg &&
+                    v < prm->min_search_cm) ||
+                   (prm->stall_limit > 0 && stalls >= prm->stall_limit);
     if (trace) {
       double *r = trace + (size_t)it * ORA_TRACE_DOUBLES;
       r[0] = Ebase; r[1] = (double)nA; r[2] = om_i; r[3] = v_i;
       memcpy(r + 4, P, 12 * sizeof(double));
       r[16] = Ec; r[17] = omega; r[18] = v;
-      r[19] = (double)((nA == 0 ? 1 : 0) | (Ebase == 1.0 ? 2 : 0));
+      r[19] = (double)((nA == 0 ? 1 : 0) | (Ebase == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0) | (rejected ? 8 : 0) |
+                       (stop ? 16 : 0));
+      r[20] = (double)nc; r[21] = (double)N; r[22] = (double)Ki; r[23] = (double)(sx + 1000 * sy);
     }
+    if (stop) { ++it; break; }
   }
+  if (trace)
+    for (; it < prm->iters; ++it) {
+      double *r = trace + (size_t)it * ORA_TRACE_DOUBLES;
+      for (int j = 0; j < ORA_TRACE_DOUBLES; ++j) r[j] = 0.0;
+      r[19] = 32.0;
+    }
   free(q_all);
   free(u_all);
   memcpy(T_out, P, sizeof P);
-  return N;
+  return N_first < 0 ? 0 : N_first;
 }
 
 /* Fitness of an arbitrary list of M poses on the frame's strided points (O1, O2, O4).

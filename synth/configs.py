@@ -35,8 +35,22 @@ class TrackParams:
     stride: int = 4               # 1/16 rate as a 4x4 stride
     min_inband_frac: float = 0.0
     delta_conv: int = 0           # 0 camera-centred (default), 1 world-literal
-    update_rule: int = 0          # 0 plain mean (paper, L14)
+    update_rule: int = 0          # 0 plain mean (paper, L14); 1 weighted (NEXT F3)
     topk: int = 0
+    nsched: int = 0               # NEXT F1: cycled (K, sx, sy) schedule
+    sched_K: tuple = (0, 0, 0, 0)
+    sched_sx: tuple = (0, 0, 0, 0)
+    sched_sy: tuple = (0, 0, 0, 0)
+    min_search_deg: float = 0.0   # F1 convergence stop; 0 = off
+    min_search_cm: float = 0.0
+    guard: int = 0                # F3 acceptance guard
+    stall_limit: int = 0          # F3 stall stop; 0 = off
+
+
+# The paper's schedule as SPEC.md:371 pairs it: largest K with the coarsest rate;
+# rates 1/32, 1/16, 1/8 as 2-D strides (8,4), (4,4), (4,2) (L20).
+PAPER_SCHEDULE = dict(nsched=3, sched_K=(10240, 3072, 1024, 0), sched_sx=(8, 4, 4, 0), sched_sy=(4, 4, 2, 0),
+                      iters=20, min_search_deg=0.1, min_search_cm=0.1)
 
 
 KINECT_VGA = Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)

@@ -1,0 +1,152 @@
+"""Pins of the oracle's NEXT-row extensions: F1 the paper's schedule
+(K and point-rate alternation, max iterations, convergence stop) and F3 the
+update-rule / acceptance variants (weighted mean w_k = E_base - E_k).
+CPU only.  Each pin is a closed form, a reduction to the already-pinned plain run, or an invariant."""
+import dataclasses
+
+import numpy as np
+
+import oracle
+from synth.configs import TrackParams, config_tiny, make_pst
+from tests.fixtures import f_track_inputs
+
+
+def _run(c, params, pst=None):
+    vol = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    return vol, vol.track(c["depth"], c["intr"], c["T_init"], c["pst"] if pst is None else pst, params)
+
+
+def test_backproject_2d_strides_brute_force():
+    """O2 with 2-D strides (sx on columns, sy on rows; L20 for the 1/8 and 1/32 rates): the list
+    equals a brute-force row-major walk over pixels (sx*c, sy*r)."""
+    c = config_tiny(seed=1)
+    depth, K = c["depth"], c["intr"]
+    for sx, sy in [(4, 2), (8, 4), (3, 5)]:
+        pts = oracle.backproject(depth, K, sx, stride_y=sy)
+        exp = []
+        for v in range(0, K.height, sy):
+            for u in range(0, K.width, sx):
+                raw = int(depth[v, u])
+                d = raw * 0.001
+                if raw > 0 and d < 8.0:
+                    exp.append(((u - K.cx) * d / K.fx, (v - K.cy) * d / K.fy, d))
+        assert np.array_equal(pts, np.array(exp))
+
+
+def test_single_entry_schedule_equals_plain_run():
+    """F1 with one schedule entry (K, s, s) is the plain run bit for bit (trace columns 0-21),
+    and records K_i and the stride code."""
+    c = config_tiny(seed=2)
+    plain = TrackParams(iters=3, stride=2)
+    sch = dataclasses.replace(plain, nsched=1, sched_K=(64, 0, 0, 0), sched_sx=(2, 0, 0, 0), sched_sy=(2, 0, 0, 0))
+    _, a = _run(c, plain)
+    _, b = _run(c, sch)
+    assert np.array_equal(a["trace"][:, :22], b["trace"][:, :22])
+    assert np.array_equal(a["T"], b["T"]) and np.array_equal(a["E"], b["E"])
+    assert np.all(b["trace"][:, 22] == 64) and np.all(b["trace"][:, 23] == 2 + 1000 * 2)
+
+
+def test_schedule_uses_template_prefix():
+    """Iteration i evaluates the first K_i template rows: a run whose schedule uses 24 of 64 rows
+    equals the plain run on the 24-row template; rows >= K_i report E = 1, n = 0."""
+    c = config_tiny(seed=3)
+    sch = TrackParams(iters=3, stride=2, nsched=1, sched_K=(24, 0, 0, 0), sched_sx=(2, 0, 0, 0), sched_sy=(2, 0, 0, 0))
+    _, a = _run(c, sch)
+    _, b = _run(c, TrackParams(iters=3, stride=2), pst=c["pst"][:24].copy())
+    assert np.array_equal(a["trace"][:, :22], b["trace"][:, :22])
+    assert np.array_equal(a["E"][:24], b["E"]) and np.all(a["E"][24:] == 1.0) and np.all(a["n"][24:] == 0)
+
+
+def test_schedule_baseline_recomputed_on_new_point_set():
+    """L11 under F1: when the point set changes, E_base of iteration i is E(P^(i-1)) on X_i (an
+    independent fitness call on the iteration's own strided points), and N_i is that set's size."""
+    c = config_tiny(seed=4)
+    sch = TrackParams(iters=4, stride=1, nsched=2, sched_K=(64, 32, 0, 0), sched_sx=(2, 4, 0, 0), sched_sy=(1, 2, 0, 0))
+    vol, r = _run(c, sch)
+    tr = r["trace"]
+    P_prev = c["T_init"]
+    for i in range(4):
+        sx, sy = (2, 1) if i % 2 == 0 else (4, 2)
+        pts = oracle.backproject(c["depth"], c["intr"], sx, stride_y=sy)
+        E, _, _ = vol.fitness(pts, P_prev)
+        assert tr[i, 0] == E and tr[i, 21] == len(pts) and tr[i, 22] == (64 if i % 2 == 0 else 32)
+        P_prev = tr[i, 4:16].reshape(3, 4)
+
+
+def test_min_search_stop():
+    """F1 convergence stop: the run stops after the first iteration whose new search size is below
+    (min_search_deg, min_search_cm); later rows are flagged not-run; T_out is that row's pose."""
+    c = config_tiny(seed=1)
+    full = TrackParams(iters=6, stride=2)
+    _, a = _run(c, full)
+    s_next = a["trace"][:, 17]
+    stop_at = int(np.argmax(s_next < 4.0))
+    assert s_next[stop_at] < 4.0 and stop_at < 5
+    _, b = _run(c, dataclasses.replace(full, min_search_deg=4.0, min_search_cm=1e9))
+    tb = b["trace"]
+    assert np.array_equal(tb[:stop_at + 1, :19], a["trace"][:stop_at + 1, :19])
+    assert int(tb[stop_at, 19]) & 16 and np.all(tb[stop_at + 1:, 19] == 32)
+    assert np.array_equal(b["T"].reshape(12), tb[stop_at, 4:16])
+
+
+def test_guard_monotone_and_rejection_keeps_pose():
+    """F3 guard: with the guard every iteration's E_c <= E_base on the same
+    point set; a rejected iteration (flag bit 3) keeps the previous pose and E_c = E_base."""
+    c = config_tiny(seed=1)
+    _, r = _run(c, TrackParams(iters=6, stride=1, guard=1))
+    tr = r["trace"]
+    assert np.all(tr[:, 16] <= tr[:, 0])
+    prev = c["T_init"].reshape(12)
+    for row in tr:
+        if int(row[19]) & 8:
+            assert np.array_equal(row[4:16], prev) and row[16] == row[0]
+        prev = row[4:16]
+    # the unguarded paper rule is not monotone on this seed; the guard matters
+    _, u = _run(c, TrackParams(iters=6, stride=1))
+    assert np.any(u["trace"][:, 16] > u["trace"][:, 0]) or np.any(tr[:, 19].astype(int) & 8)
+
+
+def test_stall_limit_on_f_track():
+    """F3 stall stop on fixture F-track: iteration 2 has an empty advantage set (a stall), so with
+    stall_limit = 1 the run stops there; with 2 it runs on."""
+    f = f_track_inputs()
+    vol = oracle.OracleVolume(f["desc"], f["V"], f["W"])
+    p = dataclasses.replace(f["params"], iters=3, stall_limit=1)
+    r = vol.track(f["depth"], f["intr"], f["T_init"], f["pst"], p)
+    tr = r["trace"]
+    assert tr[0, 1] == 1 and tr[1, 1] == 0
+    assert int(tr[1, 19]) & 16 and tr[2, 19] == 32
+    r2 = vol.track(f["depth"], f["intr"], f["T_init"], f["pst"], dataclasses.replace(p, stall_limit=2))
+    assert not (int(r2["trace"][1, 19]) & 16) and int(r2["trace"][2, 19]) & 16
+
+
+def test_weighted_mean_closed_form_on_plane():
+    """F3 weighted rule on the F-track plane: rows u_z = -2.5 cm (E = 0) and -1.25 cm
+    (E = 1.25/30) improve on E_base = 2.5/30; weights E_base - E_k give u = -2.0833 cm, while the
+    paper's plain mean gives -1.875 cm (camera-centred, t' = t + u)."""
+    f = f_track_inputs()
+    vol = oracle.OracleVolume(f["desc"], f["V"], f["W"])
+    pst = np.array([[0, 0, 0, 0, 0, -0.25], [0, 0, 0, 0, 0, -0.125]], np.float32)
+    p = dataclasses.replace(f["params"], iters=1)
+    w = vol.track(f["depth"], f["intr"], f["T_init"], pst, dataclasses.replace(p, update_rule=1))
+    m = vol.track(f["depth"], f["intr"], f["T_init"], pst, p)
+    z0 = f["T_init"][2, 3]
+    Eb, E1 = 0.025 / 0.3, 0.0125 / 0.3
+    u_w = (Eb * -0.025 + (Eb - E1) * -0.0125) / (Eb + (Eb - E1))
+    assert abs(w["T"][2, 3] - (z0 + u_w)) < 1e-7
+    assert abs(m["T"][2, 3] - (z0 - 0.01875)) < 1e-7
+    assert w["trace"][0, 1] == m["trace"][0, 1] == 2
+
+
+def test_paper_schedule_runs_and_converges_on_tiny():
+    """The paper's schedule on config T with its own K alternation (template of 10240 rows): the
+    search size never grows, K_i cycles 10240/3072/1024, and it stops by min_search within 20."""
+    from synth.configs import PAPER_SCHEDULE
+    c = config_tiny(seed=1)
+    p = TrackParams(stride=1, **PAPER_SCHEDULE)
+    _, r = _run(c, p, pst=make_pst(1, 10240))
+    tr = r["trace"]
+    ran = tr[:, 19].astype(int) & 32 == 0
+    assert np.all(np.diff(tr[ran, 2]) <= 0)
+    assert list(tr[:3, 22]) == [10240, 3072, 1024]
+    assert int(tr[ran][-1, 19]) & 16 or ran.sum() == 20
