@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PFT_ABI_VERSION 1
+#define PFT_ABI_VERSION 2
 
 typedef enum {
   PFT_OK = 0,
@@ -54,9 +54,11 @@ typedef enum { PFT_STORE_F32 = 0, PFT_STORE_F16 = 1 } pft_storage; /* value AND 
  * WORLD_LITERAL: (dR R, dR t + u), the literal left product of [dR|u] and [R|t]. */
 typedef enum { PFT_DELTA_CAMERA_CENTRED = 0, PFT_DELTA_WORLD_LITERAL = 1 } pft_delta_conv;
 
-/* Reading L14: the advantage-set average.  Only MEAN (the paper's plain mean)
- * is implemented in this version; the others return PFT_ERR_UNSUPPORTED. */
+/* Reading L14: the advantage-set average.  MEAN is the paper's plain mean;
+ * WEIGHTED (NEXT F3) weights member k by E_base - E_k > 0.  TOPK returns PFT_ERR_UNSUPPORTED. */
 typedef enum { PFT_UPDATE_MEAN = 0, PFT_UPDATE_WEIGHTED = 1, PFT_UPDATE_TOPK = 2 } pft_update_rule;
+
+#define PFT_MAX_SCHED 4
 
 typedef struct {
   int32_t nx, ny, nz;   /* voxels per axis, each >= 2                                        */
@@ -84,13 +86,28 @@ typedef struct {
   pft_delta_conv delta_conv;
   pft_update_rule update_rule;
   int32_t topk;           /* reserved for PFT_UPDATE_TOPK                                     */
+  /* NEXT F1, the paper's schedule: nsched in [1, PFT_MAX_SCHED] cycles
+   * (sched_K, sched_sx, sched_sy): iteration i uses the first min(sched_K, K) template rows and the
+   * points of column/row strides (sched_sx, sched_sy); its baseline E(P^(i-1)) is recomputed when
+   * the point set changes (reading L11).  nsched = 0: every iteration uses all rows and `stride`. */
+  int32_t nsched;
+  int32_t sched_K[PFT_MAX_SCHED], sched_sx[PFT_MAX_SCHED], sched_sy[PFT_MAX_SCHED];
+  /* F1 convergence stop: stop after an iteration whose new s has omega < min_search_deg
+   * AND v < min_search_cm (both 0: off).  Later trace rows are flagged "not run" (bit 5). */
+  double min_search_deg, min_search_cm;
+  /* NEXT F3: guard != 0 keeps P^(i-1) when E(P^(i)) > E_base (a stall,
+   * trace bit 3); stall_limit > 0 stops after that many consecutive iterations without a pose change. */
+  int32_t guard, stall_limit;
 } pft_track_params;
 
 /* Per-iteration trace record, PFT_TRACE_DOUBLES doubles:
  *  [0] E_base = E(P^(i-1))  [1] |A|  [2] omega_i (deg)  [3] v_i (cm)  [4..15] P^(i) (12)
  *  [16] E(P^(i))  [17] omega_{i+1}  [18] v_{i+1}
- *  [19] flags: bit0 advantage set empty, bit1 lost (E_base == 1), bit2 empty cloud (N == 0)
- *  [20] n_c = in-band count of P^(i)  [21] N = valid strided points  [22..23] reserved (0). */
+ *  [19] flags: bit0 advantage set empty, bit1 lost (E_base == 1), bit2 empty cloud (N == 0),
+ *       bit3 guard rejected the update, bit4 stopped after this iteration, bit5 not run
+ *  [20] n_c = in-band count of P^(i)  [21] N = valid points of the iteration's set
+ *  [22] K_i particles evaluated  [23] stride code sx + 1000 sy.
+ * Rows of iterations that did not run (after a stop) are zero except flags = 32. */
 #define PFT_TRACE_DOUBLES 24
 
 typedef struct pft_volume pft_volume; /* opaque handle */
@@ -153,6 +170,8 @@ pft_status pft_integrate_ex(pft_volume* vol, const uint16_t* dev_depth, const pf
  * (K = number of poses for pft_eval_poses). */
 pft_status pft_track_workspace_bytes(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
                                      const pft_track_params* prm, size_t* bytes_out);
+/* (E_k / n_k outputs are those of the last iteration that ran; rows k >= that iteration's K_i
+ *  report E = 1, n = 0.) */
 
 /* Randomized optimisation of PAPER.md:192-208:
  *   points: strided back-projection of the depth (stride prm->stride);

@@ -44,7 +44,10 @@ class Intrinsics(C.Structure):
 class TrackParams(C.Structure):
     _fields_ = [("omega0_deg", C.c_double), ("v0_cm", C.c_double), ("beta", C.c_double),
                 ("iters", C.c_int32), ("stride", C.c_int32), ("min_inband_frac", C.c_double),
-                ("delta_conv", C.c_int32), ("update_rule", C.c_int32), ("topk", C.c_int32)]
+                ("delta_conv", C.c_int32), ("update_rule", C.c_int32), ("topk", C.c_int32),
+                ("nsched", C.c_int32), ("sched_K", C.c_int32 * 4), ("sched_sx", C.c_int32 * 4),
+                ("sched_sy", C.c_int32 * 4), ("min_search_deg", C.c_double), ("min_search_cm", C.c_double),
+                ("guard", C.c_int32), ("stall_limit", C.c_int32)]
 
 
 _lib = None

@@ -33,8 +33,14 @@ def make_intr(k):
 
 
 def make_params(p):
+    def arr(name):
+        v = [int(x) for x in getattr(p, name, (0, 0, 0, 0))] + [0, 0, 0, 0]
+        return (C.c_int32 * 4)(*v[:4])
     return TrackParams(float(p.omega0_deg), float(p.v0_cm), float(p.beta), int(p.iters), int(p.stride),
-                       float(p.min_inband_frac), int(p.delta_conv), int(p.update_rule), int(p.topk))
+                       float(p.min_inband_frac), int(p.delta_conv), int(p.update_rule), int(p.topk),
+                       int(getattr(p, "nsched", 0)), arr("sched_K"), arr("sched_sx"), arr("sched_sy"),
+                       float(getattr(p, "min_search_deg", 0.0)), float(getattr(p, "min_search_cm", 0.0)),
+                       int(getattr(p, "guard", 0)), int(getattr(p, "stall_limit", 0)))
 
 
 def _dev_tensor(x, dtype, device):

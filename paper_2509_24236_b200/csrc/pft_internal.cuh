@@ -79,34 +79,48 @@ constexpr int kFixBits = 29;  // per-thread partial sums of <= 7 terms in [0,1) 
 // Device-resident state of one pft_track call (lives at the start of the workspace).
 struct TrackState {
   double P[12];        // current pose P^(i)
+  double Pprev[12];    // P^(i-1) (F3 guard, multi-launch path)
   double omega, v;     // current search size s^(i) (deg, cm)
-  double Ec;           // E(P) of the current pose
+  double Ec;           // E(P) of the current pose on the current point set
   double Ebase;        // E of the pose the current iteration started from
+  double Wsum;         // sum of member weights of the last update
   unsigned long long Sc_acc;  // centre accumulators (zeroed after use)
   unsigned int nc_acc;
   unsigned int nc;     // in-band count of the current pose
+  unsigned int nc_base;  // in-band count of the iteration's starting pose
   int nA;              // |A| of the last update
   int iter;            // iterations completed
-  int Nvalid;          // valid strided points
+  int Nvalid[4];       // valid points per point set (Nvalid[0]: the first iteration's set)
+  int cur_set;         // point set E_c refers to (-1: none yet)
+  int stalls;          // consecutive iterations without a pose change
+  int stopped;         // a stop rule fired: later iterations are no-ops
+  int K_last;          // K_i of the last iteration that ran
   unsigned int ticket_upd, ticket_ctr;
-  int pad0;
-  unsigned long long pmax_bits;  // max |point coordinate| of the frame (fp64 bits; persistent path)
+  unsigned long long pmax_bits;  // max |point coordinate| over all sets (persistent path)
   unsigned int bar_count, bar_gen;  // software grid barrier (persistent path)
-  double pad[6];
+  double pad[4];
 };
+
+// One strided point set (2-D strides sx on columns, sy on rows; reading L20), 8x4-pixel tiles.
+struct PointSetL { int sx, sy, nr, nc, ntx, nty, npad; size_t off; };
 
 struct TrackLayout {
   size_t state_off;
-  size_t pts_off;      // 3 * npad doubles (x, y, z SoA)
+  int nsets;
+  PointSetL sets[4];   // distinct (sx, sy) of the schedule; set of schedule entry j: sched_set[j]
+  int nsched;          // >= 1 (0 in the params maps to one entry (K, stride, stride))
+  int sched_K[4], sched_set[4];
+  int npad_max;
   size_t acc_local_off, acc_full_off;
-  size_t part_off;     // update partials: nblk_upd * 8 doubles
+  size_t part_off;     // update partials: nblk_upd * kUpdW doubles
   size_t ptab_off;     // persistent path: K x 12 folded candidate poses + K flags
   size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
   size_t work_off;     // persistent path: per-iteration work counters
   size_t total;
-  int npad, ntx, nty, nr, nc;  // point slots, tiles, strided grid rows / cols
   int kloc, kfull, nblk_upd;
 };
+
+constexpr int kUpdW = 10;  // update partial width: q(4), u(3), |A|, sum of weights, pad
 
 }  // namespace pft
 
@@ -144,5 +158,5 @@ __device__ __forceinline__ void mark_dirty_cells(const Geom& g, int bx, int by, 
 // Validation helpers shared by the entry points.
 pft_status check_intrinsics(const pft_intrinsics* K);
 pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
-                        int32_t stride, int nranks, TrackLayout* L);
+                        const pft_track_params* prm, int nranks, TrackLayout* L);
 }  // namespace pft

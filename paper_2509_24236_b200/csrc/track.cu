@@ -16,6 +16,7 @@
 // fixed-point integers (2^-29) so per-particle totals are exact and independent of order,
 // CTA shape and sharding.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "pft_internal.cuh"
@@ -153,12 +154,13 @@ __device__ __noinline__ void member_delta(const float* __restrict__ pst_row, dou
   for (int i = 0; i < 3; ++i) u[i] = uu[i];
 }
 
-// a7: P <- (R(Q/|Q|), U/|A|) P, Q and U the sums over the advantage set.
-__device__ __noinline__ void apply_mean(const double* Q, const double* U, int nA, const double* P, int conv,
+// a7: P <- (R(Q/|Q|), U/Wsum) P, Q and U the (weighted) sums over the
+// advantage set and Wsum the sum of the weights (|A| for the paper's plain mean).
+__device__ __noinline__ void apply_mean(const double* Q, const double* U, double Wsum, const double* P, int conv,
                                         double* Pn) {
   const double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
   const double qb[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
-  const double ub[3] = {U[0] / nA, U[1] / nA, U[2] / nA};
+  const double ub[3] = {U[0] / Wsum, U[1] / Wsum, U[2] / Wsum};
   double Rb[9], PP[12], out[12];
   quat_to_R(qb, Rb);
   for (int i = 0; i < 12; ++i) PP[i] = P[i];
@@ -166,14 +168,30 @@ __device__ __noinline__ void apply_mean(const double* Q, const double* U, int nA
   for (int i = 0; i < 12; ++i) Pn[i] = out[i];
 }
 
-// 256-thread fixed-shape tree over red[8][256] (result in red[c][0]); all threads must call.
-__device__ __forceinline__ void tree8(double (*red)[256], int tid) {
+// 256-thread fixed-shape tree over red[kUpdW][256] (result in red[c][0]); all threads must call.
+__device__ __forceinline__ void treeW(double (*red)[256], int tid) {
   __syncthreads();
   for (int s = 128; s > 0; s >>= 1) {
     if (tid < s)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) red[c][tid] += red[c][tid + s];
+      for (int c = 0; c < kUpdW; ++c) red[c][tid] += red[c][tid + s];
     __syncthreads();
+  }
+}
+
+// a7 contribution of particle k (E_k from its record) to one 256-particle update block:
+// member iff E_k < E_base; weight 1 (mean) or E_base - E_k (F3 weighted).
+__device__ __forceinline__ void member_row(double* row, double E, double Ebase, int rule, const float* pst_row,
+                                           double omega, double v) {
+#pragma unroll
+  for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+  if (E < Ebase) {
+    double q[4], u[3];
+    member_delta(pst_row, omega, v, q, u);
+    const double w = rule == 1 ? Ebase - E : 1.0;
+    row[0] = w * q[0]; row[1] = w * q[1]; row[2] = w * q[2]; row[3] = w * q[3];
+    row[4] = w * u[0]; row[5] = w * u[1]; row[6] = w * u[2];
+    row[7] = 1.0; row[8] = w;
   }
 }
 
@@ -430,6 +448,7 @@ template <typename T, int PPT>
 #define PFT_MINB 2
 #endif
 __global__ __launch_bounds__(kThreads, PFT_MINB) void k_particle_eval(EvalArgs a) {
+  if (a.mode == 0 && a.st->stopped) return;  // a stop rule fired (multi-launch path; uniform)
   __shared__ double2 sPose[kPC][6];
   __shared__ unsigned long long sS[kPC];
   __shared__ unsigned sN[kPC];
@@ -484,11 +503,70 @@ __device__ __forceinline__ double fitness_c(unsigned long long S, unsigned n, do
   return 1.0;
 }
 
+// ------------------------------------------------------------------ point sets and schedule
+// O1/O2 per set: pixels (sx c, sy r), r < nr = ceil(H/sy), c < nc = ceil(W/sx), in 8x4 tiles.
+struct BPFrame {
+  const uint16_t* depth;
+  double fx, fy, cx, cy, unit, max_depth;
+  int W, H;
+};
+struct PSet {
+  double *x, *y, *z;
+  int npad, sx, sy, nr, nc, ntx;
+  __host__ __device__ Points pts() const { return Points{x, y, z, npad}; }
+};
+// The iteration schedule (F1; one entry for the plain run): entry j = (K_j, point set).
+struct Sched {
+  int n, nsets;
+  int K[PFT_MAX_SCHED], set[PFT_MAX_SCHED];
+  PSet sets[PFT_MAX_SCHED];
+};
+
+__device__ __forceinline__ bool bp_slot(const BPFrame& f, const PSet& s, int i, double& X, double& Y, double& Z) {
+  const int t = i >> 5, l = i & 31;
+  const int r = (t / s.ntx) * 4 + (l >> 3), c = (t % s.ntx) * 8 + (l & 7);
+  X = Y = Z = 0.0;
+  if (r >= s.nr || c >= s.nc) return false;
+  const int u = c * s.sx, v = r * s.sy;
+  const uint16_t raw = f.depth[(size_t)v * f.W + u];
+  const double d = __dmul_rn((double)raw, f.unit);
+  if (raw == 0 || !(d < f.max_depth)) return false;
+  X = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, f.cx), d), f.fx);
+  Y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, f.cy), d), f.fy);
+  Z = d;
+  return true;
+}
+
+// Trace row of iteration `it` (include/pft.h).
+__device__ __forceinline__ void write_trace(double* r, double Ebase, int nA, double om, double v, const double* P,
+                                            double Ec, double om1, double v1, int flags, unsigned nc, int N, int Ki,
+                                            int code) {
+  r[0] = Ebase; r[1] = (double)nA; r[2] = om; r[3] = v;
+  for (int i = 0; i < 12; ++i) r[4 + i] = P[i];
+  r[16] = Ec; r[17] = om1; r[18] = v1; r[19] = (double)flags;
+  r[20] = (double)nc; r[21] = (double)N; r[22] = (double)Ki; r[23] = (double)code;
+}
+__device__ __forceinline__ void write_not_run(double* r) {
+  for (int i = 0; i < PFT_TRACE_DOUBLES; ++i) r[i] = 0.0;
+  r[19] = 32.0;
+}
+
+// a8 + F1/F3 bookkeeping shared by both implementations: s-law, stalls, stop rule.
+struct StopRule { double min_deg, min_cm; int stall_limit; };
+__device__ __forceinline__ bool stop_now(const StopRule& sr, double om1, double v1, int stalls) {
+  return ((sr.min_deg > 0.0 || sr.min_cm > 0.0) && om1 < sr.min_deg && v1 < sr.min_cm) ||
+         (sr.stall_limit > 0 && stalls >= sr.stall_limit);
+}
+__device__ __forceinline__ double s_factor(double beta, double E) {
+  // s^(i+1) = beta s^(i) + (1 - beta) E(P^(i)) s^(i), as (beta + (1-beta)E) s
+  return __dadd_rn(beta, __dmul_rn(__dsub_rn(1.0, beta), E));
+}
+
+// ------------------------------------------------------------------ multi-launch kernels (G > 1)
 struct TrackArgs {
   TrackState* st;
   const double* T_init;
-  double omega0, v0, beta, rho;
-  int conv;
+  double omega0, v0;
   PartRec* acc_local;
   int kloc;
 };
@@ -497,11 +575,13 @@ __global__ void k_track_init(TrackArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     TrackState* s = a.st;
-    for (int j = 0; j < 12; ++j) s->P[j] = a.T_init[j];
+    for (int j = 0; j < 12; ++j) { s->P[j] = a.T_init[j]; s->Pprev[j] = a.T_init[j]; }
     s->omega = a.omega0; s->v = a.v0;
-    s->Ec = 1.0; s->Ebase = 1.0;
-    s->Sc_acc = 0ull; s->nc_acc = 0u; s->nc = 0u;
-    s->nA = 0; s->iter = 0; s->Nvalid = 0;
+    s->Ec = 1.0; s->Ebase = 1.0; s->Wsum = 0.0;
+    s->Sc_acc = 0ull; s->nc_acc = 0u; s->nc = 0u; s->nc_base = 0u;
+    s->nA = 0; s->iter = 0;
+    for (int j = 0; j < 4; ++j) s->Nvalid[j] = 0;
+    s->cur_set = -1; s->stalls = 0; s->stopped = 0; s->K_last = 0;
     s->ticket_upd = 0u; s->ticket_ctr = 0u;
   }
   for (int k = i; k < a.kloc; k += gridDim.x * blockDim.x) {
@@ -511,49 +591,29 @@ __global__ void k_track_init(TrackArgs a) {
   }
 }
 
-// O1/O2: points of the strided pixel grid (sigma c, sigma r), r < nr, c < nc, in 8x4 tiles.
-struct BPArgs {
-  const uint16_t* depth;
-  double fx, fy, cx, cy, unit, max_depth;
-  int W, H, stride, nr, nc, ntx, npad;
-  double *x, *y, *z;
-  int* Nvalid;
-};
-
-__global__ void k_backproject(BPArgs a) {
+__global__ void k_backproject(BPFrame f, PSet s, int* Nvalid) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.npad) return;
-  const int t = i >> 5, l = i & 31;
-  const int r = (t / a.ntx) * 4 + (l >> 3), c = (t % a.ntx) * 8 + (l & 7);
-  double X = 0.0, Y = 0.0, Z = 0.0;
-  bool valid = false;
-  if (r < a.nr && c < a.nc) {
-    const int u = c * a.stride, v = r * a.stride;
-    const uint16_t raw = a.depth[(size_t)v * a.W + u];
-    const double d = __dmul_rn((double)raw, a.unit);
-    if (raw != 0 && d < a.max_depth) {
-      valid = true;
-      X = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, a.cx), d), a.fx);
-      Y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, a.cy), d), a.fy);
-      Z = d;
-    }
-  }
-  a.x[i] = X; a.y[i] = Y; a.z[i] = Z;
+  if (i >= s.npad) return;
+  double X, Y, Z;
+  const bool valid = bp_slot(f, s, i, X, Y, Z);
+  s.x[i] = X; s.y[i] = Y; s.z[i] = Z;
   const unsigned b = __ballot_sync(0xffffffffu, valid);
-  if (l == 0 && b) atomicAdd(a.Nvalid, __popc(b));
+  if ((i & 31) == 0 && b) atomicAdd(Nvalid, __popc(b));
 }
 
-// a5 + a8: E(P) of the current pose; the last CTA closes the iteration (s-law, trace).
+// a5 (+ a8): E(P) on point set `set`.  mode 0 (baseline, L11): E(P^(i-1)) on the iteration's set
+// when the set changed (incl. the first iteration).  mode 1 (after the update): E(P^(i)) if
+// A != {}, then the F3 guard, the s-law, stalls / stop rule and the trace row.
 struct CentreArgs {
   const void* V;                    // stored values (the centre lerps exact corner values in fp64)
   const unsigned long long* mask;
   Geom g;
   Points pts;
   TrackState* st;
-  int initial;          // 1: baseline E(T_init) before iteration 1 (no s-update, no trace)
+  int mode, set, it, Ki, code, guard;
   double beta, rho;
-  double* trace;        // NULL or iters x PFT_TRACE_DOUBLES
-  double* T_out;        // written by the last CTA of every call
+  StopRule sr;
+  double* trace;
 };
 
 template <typename T>
@@ -563,8 +623,12 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
   __shared__ bool sLast;
   __shared__ double sRed[kThreads / 32];
   TrackState* st = a.st;
-  const bool do_eval = a.initial || st->nA > 0;
   const int tid = threadIdx.x;
+  if (st->stopped) {  // uniform: a stop rule fired in an earlier iteration
+    if (a.mode == 1 && blockIdx.x == 0 && tid == 0 && a.trace) write_not_run(a.trace + (size_t)a.it * PFT_TRACE_DOUBLES);
+    return;
+  }
+  const bool do_eval = a.mode == 0 || st->nA > 0;
   if (do_eval) {
     double px[kCentrePPT], py[kCentrePPT], pz[kCentrePPT], pm = 0.0;
 #pragma unroll
@@ -605,86 +669,93 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
   if (!sLast || tid != 0) return;
   __threadfence();
   volatile TrackState* vs = st;
-  double Ec = vs->Ec;
-  unsigned nc = vs->nc;
-  if (do_eval) {
-    const unsigned long long S = vs->Sc_acc;
-    nc = vs->nc_acc;
-    Ec = fitness_c(S, nc, a.rho, vs->Nvalid);
-  }
+  const int N = vs->Nvalid[a.set];
+  const unsigned long long S = vs->Sc_acc;
+  const unsigned ncn = vs->nc_acc;
   st->Sc_acc = 0ull;
   st->nc_acc = 0u;
   st->ticket_ctr = 0u;
-  st->Ec = Ec;
-  st->nc = nc;
-  if (!a.initial) {
-    // s^(i+1) = beta s^(i) + (1 - beta) E(P^(i)) s^(i), as (beta + (1-beta)E) s
-    const double om = vs->omega, v = vs->v;
-    const double factor = __dadd_rn(a.beta, __dmul_rn(__dsub_rn(1.0, a.beta), Ec));
-    const double om1 = __dmul_rn(factor, om), v1 = __dmul_rn(factor, v);
-    st->omega = om1;
-    st->v = v1;
-    const int it = vs->iter;
-    if (a.trace) {
-      double* r = a.trace + (size_t)it * PFT_TRACE_DOUBLES;
-      const int nA = vs->nA;
-      const int N = vs->Nvalid;
-      r[0] = vs->Ebase; r[1] = (double)nA; r[2] = om; r[3] = v;
-      for (int i = 0; i < 12; ++i) r[4 + i] = vs->P[i];
-      r[16] = Ec; r[17] = om1; r[18] = v1;
-      r[19] = (double)((nA == 0 ? 1 : 0) | (vs->Ebase == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0));
-      r[20] = (double)nc; r[21] = (double)N; r[22] = 0.0; r[23] = 0.0;
-    }
-    st->iter = it + 1;
+  if (a.mode == 0) {
+    st->Ec = fitness_c(S, ncn, a.rho, N);
+    st->nc = ncn;
+    st->cur_set = a.set;
+    return;
   }
-  if (a.T_out)
-    for (int i = 0; i < 12; ++i) a.T_out[i] = vs->P[i];
+  const int nA = vs->nA;
+  const double Ebase = vs->Ebase;
+  double Ec = Ebase;
+  unsigned nc = vs->nc_base;
+  int rejected = 0;
+  if (nA > 0) {
+    const double En = fitness_c(S, ncn, a.rho, N);
+    if (a.guard && En > Ebase) {  // F3 guard: keep P^(i-1)
+      rejected = 1;
+      for (int i = 0; i < 12; ++i) st->P[i] = vs->Pprev[i];
+    } else {
+      Ec = En;
+      nc = ncn;
+    }
+  }
+  const int stalls = (nA == 0 || rejected) ? vs->stalls + 1 : 0;
+  const double om = vs->omega, v = vs->v;
+  const double f = s_factor(a.beta, Ec);
+  const double om1 = __dmul_rn(f, om), v1 = __dmul_rn(f, v);
+  const bool stop = stop_now(a.sr, om1, v1, stalls);
+  st->Ec = Ec; st->nc = nc; st->omega = om1; st->v = v1; st->stalls = stalls; st->K_last = a.Ki;
+  st->iter = a.it + 1;
+  if (stop) st->stopped = 1;
+  if (a.trace) {
+    double P[12];
+    for (int i = 0; i < 12; ++i) P[i] = vs->P[i];
+    const int flags = (nA == 0 ? 1 : 0) | (Ebase == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0) | (rejected ? 8 : 0) | (stop ? 16 : 0);
+    write_trace(a.trace + (size_t)a.it * PFT_TRACE_DOUBLES, Ebase, nA, om, v, P, Ec, om1, v1, flags, nc, N, a.Ki, a.code);
+  }
 }
 
-// a7: E_k, advantage set A = {k : E_k < E_c}, mean delta over A,
-// P <- (R(q), u) P.  nblk CTAs of 256 threads, one particle per thread; each CTA
-// reduces its members in a fixed tree, the last CTA combines the CTA partials in a fixed tree.
+// a7: E_k, advantage set A = {k < K_i : E_k < E_base}, (weighted) mean delta over A
+// (PAPER.md:206), P <- (R(q), u) P.  ceil(K_i/256) CTAs, one particle per thread;
+// each CTA reduces its members in a fixed tree, the last CTA combines the partials in a fixed tree.
 struct UpdArgs {
   TrackState* st;
   const PartRec* full;       // K records (all ranks)
   PartRec* local;            // this rank's records, zeroed for the next iteration
-  int K, k_begin, kloc;      // local covers global [k_begin, k_begin + kloc)
+  int Ki, k_begin, kloc;     // local covers global [k_begin, k_begin + kloc)
   const float* pst;
-  int conv;
+  int conv, rule, set;
   double rho;
   double* E_out;
   int* n_out;
-  double* partials;          // nblk x 8
+  double* partials;          // nblk x kUpdW
 };
 
 __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
-  __shared__ double red[8][256];
+  __shared__ double red[kUpdW][256];
   __shared__ bool sLast;
   TrackState* st = a.st;
+  if (st->stopped) return;  // uniform
   const int tid = threadIdx.x;
   const int k = blockIdx.x * 256 + tid;
-  const double Ec = st->Ec;
-  const int N = st->Nvalid;
-  double q[4] = {0.0, 0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, member = 0.0;
-  if (k < a.K) {
+  const double Ebase = st->Ec;
+  const int N = st->Nvalid[a.set];
+  double row[kUpdW];
+#pragma unroll
+  for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+  if (k < a.Ki) {
     const PartRec rec = a.full[k];
     const double E = fitness_of(rec.S, rec.n, a.rho, N);
     a.E_out[k] = E;
     a.n_out[k] = (int)rec.n;
-    if (E < Ec) {
-      member_delta(a.pst + 6 * (size_t)k, st->omega, st->v, q, u);
-      member = 1.0;
-    }
+    member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, st->omega, st->v);
     const int j = k - a.k_begin;
     if (j >= 0 && j < a.kloc) {
       a.local[j].S = 0ull;
       a.local[j].n = 0u;
     }
   }
-  red[0][tid] = q[0]; red[1][tid] = q[1]; red[2][tid] = q[2]; red[3][tid] = q[3];
-  red[4][tid] = u[0]; red[5][tid] = u[1]; red[6][tid] = u[2]; red[7][tid] = member;
-  tree8(red, tid);
-  if (tid < 8) a.partials[blockIdx.x * 8 + tid] = red[tid][0];
+#pragma unroll
+  for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
+  treeW(red, tid);
+  if (tid < kUpdW) a.partials[blockIdx.x * kUpdW + tid] = red[tid][0];
   __threadfence();
   __syncthreads();
   if (tid == 0) sLast = atomicAdd(&st->ticket_upd, 1u) == gridDim.x - 1;
@@ -693,40 +764,54 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
   __threadfence();
   // fixed-order combine of the CTA partials
 #pragma unroll
-  for (int c = 0; c < 8; ++c) red[c][tid] = 0.0;
+  for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
   for (int b = tid; b < (int)gridDim.x; b += 256)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) red[c][tid] += __ldcg(a.partials + b * 8 + c);
-  tree8(red, tid);
+    for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.partials + b * kUpdW + c);
+  treeW(red, tid);
   if (tid == 0) {
     const int nA = (int)red[7][0];
     st->nA = nA;
-    st->Ebase = Ec;
+    st->Ebase = Ebase;
+    st->nc_base = st->nc;
+    st->Wsum = red[8][0];
     st->ticket_upd = 0u;
+    for (int i = 0; i < 12; ++i) st->Pprev[i] = st->P[i];
     if (nA > 0) {
       const double Q[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
       const double U[3] = {red[4][0], red[5][0], red[6][0]};
       double Pn[12];
-      apply_mean(Q, U, nA, st->P, a.conv, Pn);
+      apply_mean(Q, U, red[8][0], st->P, a.conv, Pn);
       for (int i = 0; i < 12; ++i) st->P[i] = Pn[i];
     }
   }
 }
 
+// End of the multi-launch run: T_out; rows k >= K_last of the outputs report E = 1, n = 0.
+__global__ void k_track_finalize(const TrackState* st, int K, double* E_out, int* n_out, double* T_out) {
+  const int k0 = st->K_last;
+  for (int k = k0 + blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    E_out[k] = 1.0;
+    n_out[k] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 12) T_out[threadIdx.x] = st->P[threadIdx.x];
+}
 
 // ------------------------------------------------------------------ persistent tracker (G = 1)
 // The whole RO loop of one frame in ONE cooperative launch (all CTAs co-resident): phases are
-// separated by a software grid barrier instead of kernel boundaries, which removes ~3 launches
-// and their tail/latency per iteration.  Phase structure per iteration i:
-//   P1 candidate-pose table (K rows, each CTA a slice)                    | barrier
+// separated by a software grid barrier instead of kernel boundaries.  Per iteration i (schedule
+// entry j = i mod n, particles K_j, point set X_j):
+//   P0 (once) points of every set, pmax                                    | barrier
+//   B  baseline E(P) on X_j if the set changed (L11)                      | barrier
+//   P1 candidate-pose table (K_j rows, each CTA a slice)                  | barrier
 //   P2 particle x point evaluation: warp-granular items (4 tiles x 16
 //      particles) handed out by an atomic counter -> no CTA barriers, no
-//      wave tail; warp totals -> global integer atomics                   | barrier
+//      wave tail                                                          | barrier
 //   P3 update partials: 256-particle blocks, the same tree as k_update    | barrier
 //   P4 every CTA combines the partials in the same fixed tree (identical
-//      P everywhere), then evaluates E(P) on its slice of the points      | barrier
-//   P5 every CTA sums the centre partials (integers) -> E_c, s-law; CTA 0
-//      writes the trace.
+//      P everywhere), then evaluates E(P) on its slice of X_j             | barrier
+//   P5 every CTA: E(P), F3 guard, s-law, stalls, stop rule (identical
+//      decisions); CTA 0 writes the trace.
 // Results are bit-identical to the multi-launch path (same helpers, integer sums, same trees).
 constexpr int kItemTiles = 4;     // 8x4 tiles per warp item (= PPT 4 points per lane)
 constexpr int kItemParticles = 16;
@@ -736,11 +821,12 @@ struct PArgs {
   const void* V;
   const unsigned long long* mask;
   Geom g;
-  BPArgs bp;
-  Points pts;
+  BPFrame f;
+  Sched sc;
   const float* pst;
-  int K, conv, iters, nblk_upd, ngroups, nchunks, sched;
+  int K, conv, iters, rule, guard, sched;
   double beta, rho, omega0, v0;
+  StopRule sr;
   const double* T_init;
   TrackState* st;
   PartRec* acc;
@@ -755,8 +841,15 @@ struct PArgs {
   unsigned* work;
 };
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Sense-reversing grid barrier over co-resident CTAs; the gpu-scope fences also invalidate L1
 // (CCTL.IVALL) so data written by other CTAs before the barrier is read fresh after it.
+// Watchdog: a CTA that waits more than 5 s traps (a launch error instead of a hung GPU).
 __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -767,7 +860,14 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
       __threadfence();
       atomicExch(&st->bar_gen, gen + 1u);
     } else {
-      while (*(volatile unsigned*)&st->bar_gen == gen) __nanosleep(32);
+      const unsigned long long t0 = global_ns();
+      while (*(volatile unsigned*)&st->bar_gen == gen) {
+        __nanosleep(64);
+        if (global_ns() - t0 > 5000000000ull) {
+          printf("pft: grid barrier timeout (CTA %d, generation %u)\n", blockIdx.x, gen);
+          __trap();
+        }
+      }
     }
     __threadfence();
   }
@@ -776,14 +876,14 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
 }
 
 template <typename T>
-__device__ __forceinline__ void centre_slice(const PArgs& a, const double* m, int flag, unsigned long long& sum,
-                                             unsigned& cnt) {
-  const int per = (a.pts.npad + gridDim.x - 1) / gridDim.x;
-  const int b0 = blockIdx.x * per, b1 = min(a.pts.npad, b0 + per);
+__device__ __forceinline__ void centre_slice(const PArgs& a, const Points& pts, const double* m, int flag,
+                                             unsigned long long& sum, unsigned& cnt) {
+  const int per = (pts.npad + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(pts.npad, b0 + per);
   for (int base = b0; base < b1; base += kThreads) {
     const int i = base + threadIdx.x;
     double px[1] = {0.0}, py[1] = {0.0}, pz[1] = {0.0};
-    if (i < b1) { px[0] = __ldcg(a.pts.x + i); py[0] = __ldcg(a.pts.y + i); pz[0] = __ldcg(a.pts.z + i); }
+    if (i < b1) { px[0] = __ldcg(pts.x + i); py[0] = __ldcg(pts.y + i); pz[0] = __ldcg(pts.z + i); }
     double mm[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) mm[q] = m[q];
@@ -809,14 +909,14 @@ __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt
 template <typename T>
 __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   // red (update phases) and sPart (evaluation phase) are never live at the same time
-  constexpr size_t kRedBytes = 8 * 256 * sizeof(double);
+  constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
   constexpr size_t kPartBytes = (kThreads / 32) * kItemParticles * 33 * sizeof(unsigned long long);
   __shared__ __align__(16) unsigned char sUnion[kRedBytes > kPartBytes ? kRedBytes : kPartBytes];
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
-  __shared__ double sP[12], sM[12];
+  __shared__ double sP[12], sM[12], sPprev[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
-  __shared__ int sFlagC, sNA, sN, sItem;
-  __shared__ unsigned sNc;
+  __shared__ int sFlagC, sNA, sItem, sStalls, sStop, sSet, sKlast, sRej;
+  __shared__ unsigned sNc, sNcBase;
   __shared__ unsigned long long sS[kThreads / 32];
   __shared__ unsigned sNw[kThreads / 32];
   __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
@@ -828,67 +928,67 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned gen = 0u;
   if (tid == 0) gen = *(volatile unsigned*)&st->bar_gen;
-  // ---- P0: points (a1/a2), accumulators, pmax
+  // ---- P0: points of every set (a1/a2), accumulators, pmax
   {
     const int stride = gridDim.x * kThreads;
     double pm = 0.0;
-    for (int i0 = blockIdx.x * kThreads; i0 < a.pts.npad; i0 += stride) {
-      const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
-      const int t = i >> 5, l = i & 31;
-      const int r = (t / a.bp.ntx) * 4 + (l >> 3), c = (t % a.bp.ntx) * 8 + (l & 7);
-      double X = 0.0, Y = 0.0, Z = 0.0;
-      bool valid = false;
-      if (i < a.pts.npad && r < a.bp.nr && c < a.bp.nc) {
-        const int u = c * a.bp.stride, v = r * a.bp.stride;
-        const uint16_t raw = a.bp.depth[(size_t)v * a.bp.W + u];
-        const double d = __dmul_rn((double)raw, a.bp.unit);
-        if (raw != 0 && d < a.bp.max_depth) {
-          valid = true;
-          X = __ddiv_rn(__dmul_rn(__dsub_rn((double)u, a.bp.cx), d), a.bp.fx);
-          Y = __ddiv_rn(__dmul_rn(__dsub_rn((double)v, a.bp.cy), d), a.bp.fy);
-          Z = d;
+    for (int sidx = 0; sidx < a.sc.nsets; ++sidx) {
+      const PSet& ps = a.sc.sets[sidx];
+      for (int i0 = blockIdx.x * kThreads; i0 < ps.npad; i0 += stride) {
+        const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
+        double X = 0.0, Y = 0.0, Z = 0.0;
+        bool valid = false;
+        if (i < ps.npad) {
+          valid = bp_slot(a.f, ps, i, X, Y, Z);
+          ps.x[i] = X; ps.y[i] = Y; ps.z[i] = Z;
         }
+        pm = fmax(pm, fmax(fabs(X), fmax(fabs(Y), fabs(Z))));
+        const unsigned b = __ballot_sync(0xffffffffu, valid);
+        if (lane == 0 && b) atomicAdd(&st->Nvalid[sidx], __popc(b));
       }
-      if (i < a.pts.npad) { a.bp.x[i] = X; a.bp.y[i] = Y; a.bp.z[i] = Z; }
-      pm = fmax(pm, fmax(fabs(X), fmax(fabs(Y), fabs(Z))));
-      const unsigned b = __ballot_sync(0xffffffffu, valid);
-      if (l == 0 && b) atomicAdd(&st->Nvalid, __popc(b));
     }
     for (int sft = 16; sft > 0; sft >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, sft));
     if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
     for (int k = blockIdx.x * kThreads + tid; k < a.K; k += stride) { a.acc[k].S = 0ull; a.acc[k].n = 0u; }
   }
-  grid_barrier(st, gen);
-  const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
-  const int N = __ldcg(&st->Nvalid);
-  // ---- initial centre E(T_init)
   if (tid == 0) {
     for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
-    sFlagC = explicit_pose(sP, a.g, pmax, sM);
-  }
-  __syncthreads();
-  {
-    unsigned long long sum = 0ull;
-    unsigned cnt = 0u;
-    centre_slice<T>(a, sM, sFlagC, sum, cnt);
-    unsigned long long S;
-    unsigned n;
-    block_total(sum, cnt, sS, sNw, S, n);
-    if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
+    sState[0] = a.omega0; sState[1] = a.v0; sState[2] = 1.0;
+    sStalls = 0; sStop = 0; sSet = -1; sKlast = 0; sNc = 0u; sNA = 0;
   }
   grid_barrier(st, gen);
-  if (tid == 0) {
-    unsigned long long S = 0ull, n = 0ull;
-    for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
-    sState[0] = a.omega0; sState[1] = a.v0;
-    sState[2] = fitness_c(S, (unsigned)n, a.rho, N);
-    sNc = (unsigned)n;
-    sN = N;
-  }
-  __syncthreads();
-  for (int it = 0; it < a.iters; ++it) {
-    // ---- P1: candidate-pose table
-    for (int k = blockIdx.x * kThreads + tid; k < a.K; k += gridDim.x * kThreads) {
+  const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
+  int it = 0;
+  for (; it < a.iters; ++it) {
+    const int j = it % a.sc.n;
+    const int Ki = a.sc.K[j], set = a.sc.set[j];
+    const PSet& ps = a.sc.sets[set];
+    const Points pts = ps.pts();
+    const int N = __ldcg(&st->Nvalid[set]);
+    // ---- B: baseline E(P^(i-1)) on this iteration's point set when it changed (L11)
+    if (set != sSet) {
+      if (tid == 0) sFlagC = explicit_pose(sP, a.g, pmax, sM);
+      __syncthreads();
+      unsigned long long sum = 0ull;
+      unsigned cnt = 0u;
+      centre_slice<T>(a, pts, sM, sFlagC, sum, cnt);
+      unsigned long long S;
+      unsigned n;
+      block_total(sum, cnt, sS, sNw, S, n);
+      // half 0 of the centre partials: P5 of the previous iteration may still be reading half 1
+      if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
+      grid_barrier(st, gen);
+      if (tid == 0) {
+        unsigned long long S2 = 0ull, n2 = 0ull;
+        for (int b = 0; b < (int)gridDim.x; ++b) { S2 += __ldcg(a.cpart + 2 * b); n2 += __ldcg(a.cpart + 2 * b + 1); }
+        sState[2] = fitness_c(S2, (unsigned)n2, a.rho, N);
+        sNc = (unsigned)n2;
+        sSet = set;
+      }
+      __syncthreads();
+    }
+    // ---- P1: candidate-pose table (K_i rows)
+    for (int k = blockIdx.x * kThreads + tid; k < Ki; k += gridDim.x * kThreads) {
       double m[12];
       a.pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
       double2* row = (double2*)(a.ptab + 12 * (size_t)k);
@@ -900,7 +1000,9 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     // + chunk).  sched 0: one global dynamic queue; sched 1: CTA c owns the contiguous range
     // [c*n/G, (c+1)*n/G) (its warps share one image region -> L1 reuse), handed out by a CTA counter.
     {
-      const int nitems = a.ngroups * a.nchunks;
+      const int ngroups = (pts.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
+      const int nchunks = (Ki + kItemParticles - 1) / kItemParticles;
+      const int nitems = ngroups * nchunks;
       const int r0 = (int)((long long)nitems * blockIdx.x / gridDim.x);
       const int r1 = (int)((long long)nitems * (blockIdx.x + 1) / gridDim.x);
       if (tid == 0) sItem = 0;
@@ -910,15 +1012,15 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(a.work + it, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (a.sched == 1 ? r1 : nitems)) break;
-        const int group = item / a.nchunks, chunk = item - group * a.nchunks;
+        const int group = item / nchunks, chunk = item - group * nchunks;
         double px[kItemTiles], py[kItemTiles], pz[kItemTiles];
 #pragma unroll
         for (int p = 0; p < kItemTiles; ++p) {
           const int i = (group * kItemTiles + p) * 32 + lane;
           px[p] = py[p] = pz[p] = 0.0;
-          if (i < a.pts.npad) { px[p] = __ldcg(a.pts.x + i); py[p] = __ldcg(a.pts.y + i); pz[p] = __ldcg(a.pts.z + i); }
+          if (i < pts.npad) { px[p] = __ldcg(pts.x + i); py[p] = __ldcg(pts.y + i); pz[p] = __ldcg(pts.z + i); }
         }
-        const int k0 = chunk * kItemParticles, k1 = min(a.K, k0 + kItemParticles);
+        const int k0 = chunk * kItemParticles, k1 = min(Ki, k0 + kItemParticles);
         // stage the item's poses in this warp's shared slot (6 x 16 B per pose, 3 per lane)
         double2* wp = sWPose[tid >> 5];
         int* wf = sWFlag[tid >> 5];
@@ -964,46 +1066,48 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     }
     grid_barrier(st, gen);
     // ---- P3: E_k, advantage set, per-block partials (same tree as k_update)
-    const double Ec = sState[2];
-    for (int b = blockIdx.x; b < a.nblk_upd; b += gridDim.x) {
+    const double Ebase = sState[2];
+    const int nblk = (Ki + 255) / 256;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
       const int k = b * 256 + tid;
-      double q[4] = {0.0, 0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, member = 0.0;
-      if (k < a.K) {
+      double row[kUpdW];
+#pragma unroll
+      for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+      if (k < Ki) {
         const unsigned long long S = __ldcg(&a.acc[k].S);
         const unsigned n = __ldcg(&a.acc[k].n);
         const double E = fitness_of(S, n, a.rho, N);
         a.E_out[k] = E;
         a.n_out[k] = (int)n;
-        if (E < Ec) {
-          member_delta(a.pst + 6 * (size_t)k, sState[0], sState[1], q, u);
-          member = 1.0;
-        }
+        member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
         a.acc[k].S = 0ull;
         a.acc[k].n = 0u;
       }
-      red[0][tid] = q[0]; red[1][tid] = q[1]; red[2][tid] = q[2]; red[3][tid] = q[3];
-      red[4][tid] = u[0]; red[5][tid] = u[1]; red[6][tid] = u[2]; red[7][tid] = member;
-      tree8(red, tid);
-      if (tid < 8) a.upart[b * 8 + tid] = red[tid][0];
+#pragma unroll
+      for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
+      treeW(red, tid);
+      if (tid < kUpdW) a.upart[b * kUpdW + tid] = red[tid][0];
       __syncthreads();
     }
     grid_barrier(st, gen);
     // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
 #pragma unroll
-    for (int c = 0; c < 8; ++c) red[c][tid] = 0.0;
-    for (int b = tid; b < a.nblk_upd; b += 256)
+    for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
+    for (int b = tid; b < nblk; b += 256)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) red[c][tid] += __ldcg(a.upart + b * 8 + c);
-    tree8(red, tid);
+      for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.upart + b * kUpdW + c);
+    treeW(red, tid);
     if (tid == 0) {
       const int nA = (int)red[7][0];
       sNA = nA;
-      sState[3] = Ec;
+      sState[3] = Ebase;
+      sNcBase = sNc;
+      for (int q = 0; q < 12; ++q) sPprev[q] = sP[q];
       if (nA > 0) {
         const double Q[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
         const double U[3] = {red[4][0], red[5][0], red[6][0]};
         double Pn[12];
-        apply_mean(Q, U, nA, sP, a.conv, Pn);
+        apply_mean(Q, U, red[8][0], sP, a.conv, Pn);
         for (int q = 0; q < 12; ++q) sP[q] = Pn[q];
         sFlagC = explicit_pose(sP, a.g, pmax, sM);
       }
@@ -1012,73 +1116,117 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>(a, sM, sFlagC, sum, cnt);
+      centre_slice<T>(a, pts, sM, sFlagC, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
-      if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
+      // half 1 of the centre partials (read in P5 below; the next baseline B writes half 0)
+      unsigned long long* cp1 = a.cpart + 2 * (size_t)gridDim.x;
+      if (tid == 0) { cp1[2 * blockIdx.x] = S; cp1[2 * blockIdx.x + 1] = n; }
       grid_barrier(st, gen);  // sNA is identical in every CTA: uniform barrier
     }
-    // ---- P5: E(P), s-law, trace
+    // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
     if (tid == 0) {
-      double Ecn = sState[2];
-      unsigned nc = sNc;
+      double Ec = sState[3];
+      unsigned nc = sNcBase;
+      int rejected = 0;
       if (sNA > 0) {
+        const unsigned long long* cp1 = a.cpart + 2 * (size_t)gridDim.x;
         unsigned long long S = 0ull, n = 0ull;
-        for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(a.cpart + 2 * b); n += __ldcg(a.cpart + 2 * b + 1); }
-        nc = (unsigned)n;
-        Ecn = fitness_c(S, nc, a.rho, N);
+        for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(cp1 + 2 * b); n += __ldcg(cp1 + 2 * b + 1); }
+        const double En = fitness_c(S, (unsigned)n, a.rho, N);
+        if (a.guard && En > sState[3]) {  // F3 guard: keep P^(i-1)
+          rejected = 1;
+          for (int q = 0; q < 12; ++q) sP[q] = sPprev[q];
+        } else {
+          Ec = En;
+          nc = (unsigned)n;
+        }
       }
+      const int stalls = (sNA == 0 || rejected) ? sStalls + 1 : 0;
       const double om = sState[0], v = sState[1];
-      const double factor = __dadd_rn(a.beta, __dmul_rn(__dsub_rn(1.0, a.beta), Ecn));
-      const double om1 = __dmul_rn(factor, om), v1 = __dmul_rn(factor, v);
+      const double f = s_factor(a.beta, Ec);
+      const double om1 = __dmul_rn(f, om), v1 = __dmul_rn(f, v);
+      const bool stop = stop_now(a.sr, om1, v1, stalls);
       if (blockIdx.x == 0 && a.trace) {
-        double* r = a.trace + (size_t)it * PFT_TRACE_DOUBLES;
-        const int nA = sNA;
-        r[0] = sState[3]; r[1] = (double)nA; r[2] = om; r[3] = v;
-        for (int q = 0; q < 12; ++q) r[4 + q] = sP[q];
-        r[16] = Ecn; r[17] = om1; r[18] = v1;
-        r[19] = (double)((nA == 0 ? 1 : 0) | (sState[3] == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0));
-        r[20] = (double)nc; r[21] = (double)N; r[22] = 0.0; r[23] = 0.0;
+        const int flags = (sNA == 0 ? 1 : 0) | (sState[3] == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0) | (rejected ? 8 : 0) |
+                          (stop ? 16 : 0);
+        write_trace(a.trace + (size_t)it * PFT_TRACE_DOUBLES, sState[3], sNA, om, v, sP, Ec, om1, v1, flags, nc, N, Ki,
+                    ps.sx + 1000 * ps.sy);
       }
-      sState[0] = om1; sState[1] = v1; sState[2] = Ecn; sNc = nc;
+      sState[0] = om1; sState[1] = v1; sState[2] = Ec; sNc = nc; sStalls = stalls; sStop = stop ? 1 : 0;
+      sKlast = Ki; sRej = rejected;
     }
     __syncthreads();
+    if (sStop) { ++it; break; }  // identical decision in every CTA
   }
+  // ---- outputs
   if (blockIdx.x == 0 && tid == 0) {
     for (int q = 0; q < 12; ++q) { a.T_out[q] = sP[q]; st->P[q] = sP[q]; }
     st->omega = sState[0]; st->v = sState[1]; st->Ec = sState[2]; st->nA = sNA; st->nc = sNc;
-    st->iter = a.iters;
+    st->iter = it; st->K_last = sKlast; st->stopped = sStop;
+    if (a.trace)
+      for (int r = it; r < a.iters; ++r) write_not_run(a.trace + (size_t)r * PFT_TRACE_DOUBLES);
+  }
+  for (int k = sKlast + blockIdx.x * kThreads + tid; k < a.K; k += gridDim.x * kThreads) {
+    a.E_out[k] = 1.0;
+    a.n_out[k] = 0;
   }
 }
 
 // ------------------------------------------------------------------ host side
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles, int32_t stride,
-                        int nranks, TrackLayout* L) {
+pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
+                        const pft_track_params* prm, int nranks, TrackLayout* L) {
   (void)vol;
   if (nparticles < 1) return fail(PFT_ERR_INVALID_ARG, "number of particles/poses must be >= 1");
-  if (stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
+  if (prm->stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
+  if (prm->nsched < 0 || prm->nsched > PFT_MAX_SCHED) return fail(PFT_ERR_INVALID_ARG, "nsched must be in [0,%d]", PFT_MAX_SCHED);
   pft_status s = check_intrinsics(K);
   if (s != PFT_OK) return s;
-  L->nr = (K->height + stride - 1) / stride;
-  L->nc = (K->width + stride - 1) / stride;
-  L->ntx = (L->nc + 7) / 8;
-  L->nty = (L->nr + 3) / 4;
-  L->npad = L->ntx * L->nty * 32;
+  int n = prm->nsched > 0 ? prm->nsched : 1;
+  L->nsched = n;
+  L->nsets = 0;
+  L->npad_max = 0;
+  size_t off = 0;
+  L->state_off = off; off = align_up(off + sizeof(TrackState), 256);
+  for (int j = 0; j < n; ++j) {
+    int sx = prm->stride, sy = prm->stride, Kj = nparticles;
+    if (prm->nsched > 0) {
+      sx = prm->sched_sx[j]; sy = prm->sched_sy[j];
+      if (prm->sched_K[j] < 1) return fail(PFT_ERR_INVALID_ARG, "sched_K[%d] must be >= 1", j);
+      Kj = prm->sched_K[j] < nparticles ? prm->sched_K[j] : nparticles;
+    }
+    if (sx < 1 || sy < 1) return fail(PFT_ERR_INVALID_ARG, "schedule strides must be >= 1");
+    L->sched_K[j] = Kj;
+    int found = -1;
+    for (int q = 0; q < L->nsets; ++q)
+      if (L->sets[q].sx == sx && L->sets[q].sy == sy) found = q;
+    if (found < 0) {
+      PointSetL& p = L->sets[L->nsets];
+      p.sx = sx; p.sy = sy;
+      p.nr = (K->height + sy - 1) / sy;
+      p.nc = (K->width + sx - 1) / sx;
+      p.ntx = (p.nc + 7) / 8;
+      p.nty = (p.nr + 3) / 4;
+      p.npad = p.ntx * p.nty * 32;
+      p.off = off;
+      off = align_up(off + 3 * sizeof(double) * (size_t)p.npad, 256);
+      if (p.npad > L->npad_max) L->npad_max = p.npad;
+      found = L->nsets++;
+    }
+    L->sched_set[j] = found;
+  }
   L->kloc = (nparticles + nranks - 1) / nranks;
   L->kfull = L->kloc * nranks;
   L->nblk_upd = (nparticles + 255) / 256;
-  size_t off = 0;
-  L->state_off = off; off = align_up(off + sizeof(TrackState), 256);
-  L->pts_off = off; off = align_up(off + 3 * sizeof(double) * (size_t)L->npad, 256);
   L->acc_local_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kloc, 256);
   if (nranks > 1) { L->acc_full_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kfull, 256); }
   else L->acc_full_off = L->acc_local_off;
-  L->part_off = off; off = align_up(off + 8 * sizeof(double) * (size_t)L->nblk_upd, 256);
+  L->part_off = off; off = align_up(off + kUpdW * sizeof(double) * (size_t)L->nblk_upd, 256);
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
-  L->cpart_off = off; off = align_up(off + 2 * sizeof(unsigned long long) * 148 * 8, 256);
+  L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
   L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024, 256);
   L->total = off;
   return PFT_OK;
@@ -1092,42 +1240,62 @@ struct Launch {
   char* ws;
   cudaStream_t st;
   TrackState* state() const { return (TrackState*)(ws + L.state_off); }
-  Points pts() const {
-    double* p = (double*)(ws + L.pts_off);
-    return Points{p, p + L.npad, p + 2 * (size_t)L.npad, L.npad};
+  PSet set(int q) const {
+    const PointSetL& p = L.sets[q];
+    double* b = (double*)(ws + p.off);
+    return PSet{b, b + p.npad, b + 2 * (size_t)p.npad, p.npad, p.sx, p.sy, p.nr, p.nc, p.ntx};
+  }
+  Sched sched() const {
+    Sched s;
+    s.n = L.nsched;
+    s.nsets = L.nsets;
+    for (int j = 0; j < PFT_MAX_SCHED; ++j) { s.K[j] = j < L.nsched ? L.sched_K[j] : 0; s.set[j] = j < L.nsched ? L.sched_set[j] : 0; }
+    for (int q = 0; q < PFT_MAX_SCHED; ++q) s.sets[q] = q < L.nsets ? set(q) : PSet{};
+    return s;
   }
 };
 
-static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_intrinsics* K, int stride,
-                            const double* T_init, double omega0, double v0, int conv) {
-  TrackArgs ta{c.state(), T_init, omega0, v0, 0.0, 0.0, conv, (PartRec*)(c.ws + c.L.acc_local_off), c.L.kloc};
+static BPFrame frame_of(const Launch& c, const uint16_t* depth, const pft_intrinsics* K) {
+  return BPFrame{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height};
+}
+
+static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
+                            double omega0, double v0) {
+  TrackArgs ta{c.state(), T_init, omega0, v0, (PartRec*)(c.ws + c.L.acc_local_off), c.L.kloc};
   int gi = (c.L.kloc + 255) / 256;
   PFT_LAUNCH(PFT_PROF_PREP, c.st, k_track_init<<<gi < 148 ? gi : 148, 256, 0, c.st>>>(ta));
-  Points P = c.pts();
-  BPArgs b{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height, stride,
-           c.L.nr, c.L.nc, c.L.ntx, c.L.npad, (double*)P.x, (double*)P.y, (double*)P.z, &c.state()->Nvalid};
-  PFT_LAUNCH(PFT_PROF_PREP, c.st, k_backproject<<<(c.L.npad + 255) / 256, 256, 0, c.st>>>(b));
+  const BPFrame f = frame_of(c, depth, K);
+  for (int q = 0; q < c.L.nsets; ++q) {
+    const PSet s = c.set(q);
+    PFT_LAUNCH(PFT_PROF_PREP, c.st, k_backproject<<<(s.npad + 255) / 256, 256, 0, c.st>>>(f, s, &c.state()->Nvalid[q]));
+  }
 }
 
 template <typename T>
-static void launch_centre(const Launch& c, int initial, double beta, double rho, double* trace, double* T_out) {
-  CentreArgs ca{c.vol->base + c.vol->L.v_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), c.state(), initial, beta, rho, trace, T_out};
-  int grid = (c.L.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
+static void launch_centre(const Launch& c, int mode, int set, int it, int Ki, const pft_track_params* prm,
+                          double* trace) {
+  const PSet s = c.set(set);
+  CentreArgs ca{c.vol->base + c.vol->L.v_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g,
+                s.pts(), c.state(), mode, set, it, Ki, s.sx + 1000 * s.sy, prm->guard, prm->beta,
+                prm->min_inband_frac, StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit}, trace};
+  int grid = (s.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
   PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
 }
 
 template <typename T>
 static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin, int k_count, int conv,
-                        const double* poses, PartRec* acc) {
+                        const double* poses, PartRec* acc, int set) {
   if (k_count <= 0) return;
-  EvalArgs ea{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g, c.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
-  dim3 grid((c.L.npad + kThreads * kPPT - 1) / (kThreads * kPPT), (k_count + kPC - 1) / kPC);
+  const PSet s = c.set(set);
+  EvalArgs ea{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g,
+              s.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
+  dim3 grid((s.npad + kThreads * kPPT - 1) / (kThreads * kPPT), (k_count + kPC - 1) / kPC);
   static const int ppt = [] {  // tuning knob for experiments: PFT_EVAL_PPT=2|4
     const char* e = getenv("PFT_EVAL_PPT");
     return e && atoi(e) == 2 ? 2 : kPPT;
   }();
   if (ppt == 2) {
-    grid.x = (c.L.npad + kThreads * 2 - 1) / (kThreads * 2);
+    grid.x = (s.npad + kThreads * 2 - 1) / (kThreads * 2);
     PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, 2><<<grid, kThreads, 0, c.st>>>(ea));
   } else {
     PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, kPPT><<<grid, kThreads, 0, c.st>>>(ea));
@@ -1151,23 +1319,19 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   }
   cudaMemsetAsync(c.state(), 0, sizeof(TrackState), c.st);
   cudaMemsetAsync(c.ws + c.L.work_off, 0, sizeof(unsigned) * (size_t)prm->iters, c.st);
-  Points P = c.pts();
   PArgs pa;
   pa.R = c.vol->base + c.vol->L.r_off;
   pa.V = c.vol->base + c.vol->L.v_off;
   pa.mask = (const unsigned long long*)(c.vol->base + c.vol->L.m_off);
   pa.g = c.vol->g;
-  pa.bp = BPArgs{depth, K->fx, K->fy, K->cx, K->cy, K->depth_unit_m, c.vol->g.max_depth, K->width, K->height,
-                 prm->stride, c.L.nr, c.L.nc, c.L.ntx, c.L.npad, (double*)P.x, (double*)P.y, (double*)P.z,
-                 &c.state()->Nvalid};
-  pa.pts = P;
+  pa.f = frame_of(c, depth, K);
+  pa.sc = c.sched();
   pa.pst = pst;
-  pa.K = Kp; pa.conv = prm->delta_conv; pa.iters = prm->iters; pa.nblk_upd = c.L.nblk_upd;
-  pa.ngroups = (c.L.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
-  pa.nchunks = (Kp + kItemParticles - 1) / kItemParticles;
+  pa.K = Kp; pa.conv = prm->delta_conv; pa.iters = prm->iters; pa.rule = prm->update_rule; pa.guard = prm->guard;
   static const int sched = [] { const char* e = getenv("PFT_EVAL_SCHED"); return e ? atoi(e) : 0; }();
   pa.sched = sched;
   pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
+  pa.sr = StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit};
   pa.T_init = T_init;
   pa.st = c.state();
   pa.acc = (PartRec*)(c.ws + c.L.acc_local_off);
@@ -1202,22 +1366,27 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
     return track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
   const int kloc = c.L.kloc;
   const int k_begin = r * kloc;
-  const int k_count = max(0, min(Kp, k_begin + kloc) - k_begin);
   PartRec* local = (PartRec*)(c.ws + c.L.acc_local_off);
   PartRec* full = (PartRec*)(c.ws + c.L.acc_full_off);
-  launch_prologue(c, depth, K, prm->stride, T_init, prm->omega0_deg, prm->v0_cm, prm->delta_conv);
-  launch_centre<T>(c, 1, prm->beta, prm->min_inband_frac, nullptr, nullptr);
+  launch_prologue(c, depth, K, T_init, prm->omega0_deg, prm->v0_cm);
+  int prev_set = -1;
   for (int it = 0; it < prm->iters; ++it) {
-    launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local);
+    const int j = it % c.L.nsched;
+    const int Ki = c.L.sched_K[j], set = c.L.sched_set[j];
+    if (set != prev_set) launch_centre<T>(c, 0, set, it, Ki, prm, trace);  // baseline on the new set (L11)
+    prev_set = set;
+    const int k_count = max(0, min(Ki, k_begin + kloc) - k_begin);
+    launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local, set);
     if (G > 1) {
       pft_status s = comm_allgather(c.vol, local, full, sizeof(PartRec) * (size_t)kloc, c.st);
       if (s != PFT_OK) return s;
     }
-    UpdArgs ua{c.state(), full, local, Kp, k_begin, kloc, pst, prm->delta_conv, prm->min_inband_frac, E, n_out,
-               (double*)(c.ws + c.L.part_off)};
-    PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_update<<<c.L.nblk_upd, 256, 0, c.st>>>(ua));
-    launch_centre<T>(c, 0, prm->beta, prm->min_inband_frac, trace, it == prm->iters - 1 ? T_out : nullptr);
+    UpdArgs ua{c.state(), full, local, Ki, k_begin, kloc, pst, prm->delta_conv, prm->update_rule, set,
+               prm->min_inband_frac, E, n_out, (double*)(c.ws + c.L.part_off)};
+    PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_update<<<(Ki + 255) / 256, 256, 0, c.st>>>(ua));
+    launch_centre<T>(c, 1, set, it, Ki, prm, trace);
   }
+  PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_track_finalize<<<(Kp + 255) / 256, 256, 0, c.st>>>(c.state(), Kp, E, n_out, T_out));
   return cuda_check("track");
 }
 
@@ -1226,7 +1395,7 @@ __global__ void k_finish_poses(const PartRec* acc, int M, const TrackState* st, 
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= M) return;
   const PartRec r = acc[k];
-  E[k] = fitness_of(r.S, r.n, rho, st->Nvalid);
+  E[k] = fitness_of(r.S, r.n, rho, st->Nvalid[0]);
   n[k] = (int)r.n;
 }
 
@@ -1240,7 +1409,12 @@ static pft_status check_params(const pft_track_params* p) {
   if (!(p->min_inband_frac >= 0.0 && p->min_inband_frac <= 1.0)) return fail(PFT_ERR_INVALID_ARG, "min_inband_frac must be in [0,1]");
   if (p->delta_conv != PFT_DELTA_CAMERA_CENTRED && p->delta_conv != PFT_DELTA_WORLD_LITERAL)
     return fail(PFT_ERR_INVALID_ARG, "bad delta_conv");
-  if (p->update_rule != PFT_UPDATE_MEAN) return fail(PFT_ERR_UNSUPPORTED, "only PFT_UPDATE_MEAN is implemented");
+  if (p->update_rule == PFT_UPDATE_TOPK) return fail(PFT_ERR_UNSUPPORTED, "PFT_UPDATE_TOPK is not implemented");
+  if (p->update_rule != PFT_UPDATE_MEAN && p->update_rule != PFT_UPDATE_WEIGHTED)
+    return fail(PFT_ERR_INVALID_ARG, "bad update_rule");
+  if (p->nsched < 0 || p->nsched > PFT_MAX_SCHED) return fail(PFT_ERR_INVALID_ARG, "nsched must be in [0,%d]", PFT_MAX_SCHED);
+  if (!(p->min_search_deg >= 0.0) || !(p->min_search_cm >= 0.0)) return fail(PFT_ERR_INVALID_ARG, "min_search must be >= 0");
+  if (p->stall_limit < 0) return fail(PFT_ERR_INVALID_ARG, "stall_limit must be >= 0");
   return PFT_OK;
 }
 
@@ -1254,7 +1428,7 @@ pft_status pft_track_workspace_bytes(const pft_volume* vol, const pft_intrinsics
                                      const pft_track_params* prm, size_t* bytes_out) {
   if (!vol || !bytes_out || !prm) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
   TrackLayout L;
-  pft_status s = track_layout(vol, K, nparticles, prm->stride, vol->nranks, &L);
+  pft_status s = track_layout(vol, K, nparticles, prm, vol->nranks, &L);
   if (s != PFT_OK) return s;
   *bytes_out = L.total;
   return PFT_OK;
@@ -1272,7 +1446,7 @@ pft_status pft_track(pft_volume* vol, const uint16_t* dev_depth, const pft_intri
   c.vol = vol;
   c.ws = (char*)dev_ws;
   c.st = (cudaStream_t)stream;
-  s = track_layout(vol, K, nparticles, prm->stride, vol->nranks, &c.L);
+  s = track_layout(vol, K, nparticles, prm, vol->nranks, &c.L);
   if (s != PFT_OK) return s;
   if (ws_bytes < c.L.total) return fail(PFT_ERR_BUFFER_TOO_SMALL, "workspace %zu B < required %zu B", ws_bytes, c.L.total);
   if (((uintptr_t)dev_ws) % 256) return fail(PFT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
@@ -1292,16 +1466,18 @@ pft_status pft_eval_poses(const pft_volume* vol, const uint16_t* dev_depth, cons
   c.vol = (pft_volume*)vol;
   c.ws = (char*)dev_ws;
   c.st = (cudaStream_t)stream;
-  // eval_poses is rank-local: lay the workspace out for one rank
-  pft_status s = track_layout(vol, K, M, prm->stride, 1, &c.L);
+  // eval_poses is rank-local and uses the plain stride (no schedule)
+  pft_track_params p1 = *prm;
+  p1.nsched = 0;
+  pft_status s = track_layout(vol, K, M, &p1, 1, &c.L);
   if (s != PFT_OK) return s;
   if (ws_bytes < c.L.total) return fail(PFT_ERR_BUFFER_TOO_SMALL, "workspace %zu B < required %zu B", ws_bytes, c.L.total);
   if (((uintptr_t)dev_ws) % 256) return fail(PFT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   // (the state's pose is initialised from pose 0; eval_poses never reads it)
-  launch_prologue(c, dev_depth, K, prm->stride, dev_poses, 0.0, 0.0, 0);
+  launch_prologue(c, dev_depth, K, dev_poses, 0.0, 0.0);
   PartRec* acc = (PartRec*)(c.ws + c.L.acc_local_off);
-  if (vol->esize == 4) launch_eval<float>(c, 1, nullptr, 0, M, 0, dev_poses, acc);
-  else launch_eval<__half>(c, 1, nullptr, 0, M, 0, dev_poses, acc);
+  if (vol->esize == 4) launch_eval<float>(c, 1, nullptr, 0, M, 0, dev_poses, acc, 0);
+  else launch_eval<__half>(c, 1, nullptr, 0, M, 0, dev_poses, acc, 0);
   PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_finish_poses<<<(M + 255) / 256, 256, 0, c.st>>>(acc, M, c.state(), prm->min_inband_frac, dev_E, dev_inband));
   return cuda_check("eval_poses");
 }
@@ -1311,7 +1487,7 @@ pft_status pft_track_info(const void* dev_ws, int32_t* npoints_out, void* stream
   cudaStream_t st = (cudaStream_t)stream;
   int n = 0;
   const TrackState* s = (const TrackState*)dev_ws;  // state is at offset 0 of every layout
-  if (cudaMemcpyAsync(&n, &s->Nvalid, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+  if (cudaMemcpyAsync(&n, &s->Nvalid[0], sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return cuda_check("track_info");
   *npoints_out = n;

@@ -12,7 +12,12 @@ def main(cfg, seed, out):
     import torch
     import paper_2509_24236_b200 as pft
     from synth.configs import config_single, config_tiny, with_desc
+    import dataclasses
     c = config_tiny(seed=seed) if cfg.startswith("tiny") else config_single(seed=seed)
+    if cfg == "tiny_sched":
+        c["params"] = dataclasses.replace(c["params"], iters=7, nsched=3, sched_K=(64, 40, 24, 0),
+                                          sched_sx=(1, 2, 4, 0), sched_sy=(1, 2, 2, 0), guard=1, update_rule=1,
+                                          stall_limit=3, min_search_deg=0.05, min_search_cm=0.05)
     if cfg == "tiny16":
         c = with_desc(c, storage="f16")
         c["V"], c["W"] = c["V"].astype(np.float16), c["W"].astype(np.float16)

@@ -310,7 +310,7 @@ def test_sequence_track_then_integrate(pft):
     vol.close()
 
 
-@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single"])
+@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single", "tiny_sched"])
 def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
     """The single-launch persistent tracker (G = 1 default) and the multi-launch path (used for
     G > 1) share their arithmetic helpers and fixed reduction trees: outputs must be bit-identical."""
@@ -325,3 +325,53 @@ def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
         outs[mode] = np.load(f)
     for k in ("T", "E", "n", "trace"):
         assert np.array_equal(outs["0"][k], outs["1"][k]), k
+
+
+# ------------------------------------------------------------------ NEXT rows F1 / F3
+SCHED_TINY = dict(nsched=3, sched_K=(64, 40, 24, 0), sched_sx=(2, 2, 4, 0), sched_sy=(1, 2, 2, 0))
+
+
+@pytest.mark.parametrize("variant", ["schedule", "schedule_guard", "weighted", "weighted_guard_world"])
+def test_track_next_rows_tiny(pft, variant):
+    """F1 (cycled K / 2-D stride schedule, baseline recomputed on a new point set) and F3 (guard,
+    weighted mean) against the oracle: every iteration's trace row and the last E_k / n_k."""
+    import dataclasses
+    c = config_tiny(seed=2)
+    base = TrackParams(iters=7, stride=1)
+    kw = {"schedule": dict(SCHED_TINY), "schedule_guard": dict(SCHED_TINY, guard=1),
+          "weighted": dict(update_rule=1), "weighted_guard_world": dict(update_rule=1, guard=1, delta_conv=1)}[variant]
+    params = dataclasses.replace(base, **kw)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], params)
+    ov = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    o = ov.track(c["depth"], c["intr"], c["T_init"], c["pst"], params)
+    assert_trace_parity(r["trace"], o["trace"], variant)
+    np.testing.assert_array_equal(r["trace"][:, 20:24], o["trace"][:, 20:24])
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], c["pst"], params, c["T_init"], variant)
+    assert_pose_close(r["T"], o["T"], variant)
+    vol.close()
+
+
+@pytest.mark.parametrize("stop", ["min_search", "stall"])
+def test_track_stop_rules(pft, stop):
+    """F1 min-search stop and F3 stall stop: the same stop iteration as the oracle, later trace rows
+    flagged not-run (bit 5), T_out = the last row's pose."""
+    import dataclasses
+    if stop == "stall":
+        f = f_track_inputs()
+        desc, V, W, depth, intr, T0, pst = f["desc"], f["V"], f["W"], f["depth"], f["intr"], f["T_init"], f["pst"]
+        params = dataclasses.replace(f["params"], iters=4, stall_limit=1)
+    else:
+        c = config_tiny(seed=1)
+        desc, V, W, depth, intr, T0, pst = c["desc"], c["V"], c["W"], c["depth"], c["intr"], c["T_init"], c["pst"]
+        params = TrackParams(iters=8, stride=2, min_search_deg=4.0, min_search_cm=1e9)
+    vol = gpu_volume(pft, desc, V, W)
+    r = run_track(pft, vol, depth, intr, T0, pst, params)
+    o = oracle.OracleVolume(desc, V, W).track(depth, intr, T0, pst, params)
+    ran = (o["trace"][:, 19].astype(int) & 32) == 0
+    assert 0 < ran.sum() < params.iters
+    assert np.array_equal(r["trace"][:, 19], o["trace"][:, 19])
+    assert_trace_parity(r["trace"][ran], o["trace"][ran], stop)
+    assert np.all(r["trace"][~ran] == o["trace"][~ran])
+    assert_pose_close(r["T"], o["T"], stop)
+    vol.close()
