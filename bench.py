@@ -199,7 +199,7 @@ def run_ours(args):
     # ---- end-to-end through the public API with host buffers
     host_depth = [torch.from_numpy(s["depth"]).pin_memory() for s in steps_in]
     host_tinit = [torch.from_numpy(s["T_init"]).pin_memory() for s in steps_in]
-    host_T = torch.empty(3, 4, dtype=torch.float64).pin_memory()
+    host_T = [torch.empty(3, 4, dtype=torch.float64).pin_memory() for _ in idx]
     d_buf = torch.empty_like(depth_dev[0])
     t_buf = torch.empty_like(tinit_dev[0])
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
@@ -210,9 +210,16 @@ def run_ours(args):
         d_buf.copy_(host_depth[i], non_blocking=True)
         t_buf.copy_(host_tinit[i], non_blocking=True)
         step(i, d_buf, t_buf)
-        host_T.copy_(out["T"], non_blocking=True)
+        host_T[j].copy_(out["T"], non_blocking=True)
         ev2[j][1].record(stream)
     barrier()
+    # tracked pose vs GT per frame (characterisation of the paper-literal rule)
+    rot_err, tr_err = [], []
+    for j, i in enumerate(idx):
+        Tg, Tt = seq.gt[steps_in[i]["t"]], host_T[j].numpy()
+        c = (np.trace(Tg[:, :3].T @ Tt[:, :3]) - 1.0) / 2.0
+        rot_err.append(float(np.degrees(np.arccos(np.clip(c, -1.0, 1.0)))))
+        tr_err.append(float(np.linalg.norm(Tg[:, 3] - Tt[:, 3]) * 100.0))
     e2e_ms = sum(a.elapsed_time(b) for a, b in ev2)
     if world > 1:
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
@@ -239,6 +246,31 @@ def run_ours(args):
         tj = json.load(open(tf))
         traffic = tj.get("dram_bytes_per_eval", 0) * evals_per_launch
 
+    # ---- particle sweep (BASELINE config 4 sizes) on the same 512^3 map, one frame, 10 iterations
+    sweep = {}
+    if world == 1:
+        for Ks in (4096, 16384, 65536):
+            from synth.configs import make_pst
+            pst_s = torch.from_numpy(make_pst(args.seed, Ks)).to(dev)
+            o2 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev),
+                      E=torch.empty(Ks, dtype=torch.float64, device=dev), n=torch.empty(Ks, dtype=torch.int32, device=dev),
+                      trace=None)
+            i0 = idx[0]
+            vol.track(depth_dev[i0], intr, tinit_dev[i0], pst_s, params, out=o2)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(3):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                vol.track(depth_dev[i0], intr, tinit_dev[i0], pst_s, params, out=o2)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            sweep[str(Ks)] = {"evals_per_s": Ks * n_valid[i0] * ITERS / (min(ts) * 1e-3), "ms_track": min(ts)}
+            del pst_s, o2
+        vol._ws = {}
+
     res = {
         "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
         "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -261,6 +293,10 @@ def run_ours(args):
                               "gathers are L2/L1-resident (DESIGN.md §7)",
                      "evals_per_s_kernel": evals_per_launch / avg_launch_s},
         "clocks": clk.summary(),
+        "particle_sweep": sweep,
+        "pose_err_vs_gt": {"rot_deg_median": statistics.median(rot_err), "rot_deg_p90": float(np.percentile(rot_err, 90)),
+                           "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),
+                           "note": "paper-literal RO from GT (+) U+-5deg/+-5cm, per frame (SURVEY.md 8(c-5))"},
     }
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(args, seq, map_depth, [steps_in[i] for i in idx])

@@ -876,7 +876,8 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
 }
 
 template <typename T>
-__device__ __forceinline__ void centre_slice(const PArgs& a, const Points& pts, const double* m, int flag,
+__device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsigned long long* __restrict__ mask,
+                                             const Geom& g, const Points& pts, const double* m, int flag,
                                              unsigned long long& sum, unsigned& cnt) {
   const int per = (pts.npad + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(pts.npad, b0 + per);
@@ -887,8 +888,8 @@ __device__ __forceinline__ void centre_slice(const PArgs& a, const Points& pts, 
     double mm[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) mm[q] = m[q];
-    if (flag == 2) eval_points_f64<T, true, 1>((const T*)a.V, a.mask, a.g, mm, px, py, pz, sum, cnt);
-    else if (flag == 1) eval_points_f64<T, false, 1>((const T*)a.V, a.mask, a.g, mm, px, py, pz, sum, cnt);
+    if (flag == 2) eval_points_f64<T, true, 1>(V, mask, g, mm, px, py, pz, sum, cnt);
+    else if (flag == 1) eval_points_f64<T, false, 1>(V, mask, g, mm, px, py, pz, sum, cnt);
   }
 }
 
@@ -924,16 +925,30 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   // per-lane partials of the item's particles: (fix | cnt << 32), rows padded against bank conflicts
   unsigned long long (*sPart)[kItemParticles][33] =
       reinterpret_cast<unsigned long long (*)[kItemParticles][33]>(sUnion);
+  // the schedule lives in shared memory: dynamically indexing the kernel-parameter copy would
+  // make the compiler spill the whole parameter block to local memory
+  __shared__ PSet sSets[PFT_MAX_SCHED];
+  __shared__ int sSchedK[PFT_MAX_SCHED], sSchedSet[PFT_MAX_SCHED];
   TrackState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned gen = 0u;
-  if (tid == 0) gen = *(volatile unsigned*)&st->bar_gen;
+  if (tid == 0) {
+    gen = *(volatile unsigned*)&st->bar_gen;
+#pragma unroll
+    for (int q = 0; q < PFT_MAX_SCHED; ++q) {
+      sSets[q] = a.sc.sets[q];
+      sSchedK[q] = a.sc.K[q];
+      sSchedSet[q] = a.sc.set[q];
+    }
+  }
+  __syncthreads();
+  const int nsched = a.sc.n, nsets = a.sc.nsets;
   // ---- P0: points of every set (a1/a2), accumulators, pmax
   {
     const int stride = gridDim.x * kThreads;
     double pm = 0.0;
-    for (int sidx = 0; sidx < a.sc.nsets; ++sidx) {
-      const PSet& ps = a.sc.sets[sidx];
+    for (int sidx = 0; sidx < nsets; ++sidx) {
+      const PSet ps = sSets[sidx];
       for (int i0 = blockIdx.x * kThreads; i0 < ps.npad; i0 += stride) {
         const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
         double X = 0.0, Y = 0.0, Z = 0.0;
@@ -960,9 +975,9 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
   int it = 0;
   for (; it < a.iters; ++it) {
-    const int j = it % a.sc.n;
-    const int Ki = a.sc.K[j], set = a.sc.set[j];
-    const PSet& ps = a.sc.sets[set];
+    const int j = it % nsched;
+    const int Ki = sSchedK[j], set = sSchedSet[j];
+    const PSet ps = sSets[set];
     const Points pts = ps.pts();
     const int N = __ldcg(&st->Nvalid[set]);
     // ---- B: baseline E(P^(i-1)) on this iteration's point set when it changed (L11)
@@ -971,7 +986,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       __syncthreads();
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>(a, pts, sM, sFlagC, sum, cnt);
+      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
@@ -1116,7 +1131,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>(a, pts, sM, sFlagC, sum, cnt);
+      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
