@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--map-frames", type=int, default=8)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-large", action="store_true", help="skip the config-L (1024^3 fp16) measurement")
     return p.parse_args()
 
 
@@ -271,6 +272,45 @@ def run_ours(args):
             del pst_s, o2
         vol._ws = {}
 
+    # ---- config L: 1024^3 @ 5 mm fp16 volume built by integration, K = 4096 track + integrate per frame
+    large = {}
+    if world == 1 and not args.no_large:
+        from synth.configs import Sequence
+        sl = Sequence("L", seed=args.seed, n_frames=max(len(map_depth) + 8, 16), K=4096, iters=ITERS)
+        voll = pft.Volume(sl.desc, dev)
+        voll.reset()
+        for t in range(len(map_depth)):
+            voll.integrate(torch.from_numpy(sl.depth(t)).to(dev), sl.intr, torch.from_numpy(sl.gt[t].copy()).to(dev))
+        pst_l = torch.from_numpy(sl.pst).to(dev)
+        frames = [len(map_depth) + f for f in range(6)]
+        dl = [torch.from_numpy(sl.depth(t)).to(dev) for t in frames]
+        from synth.configs import init_noise
+        tl = [torch.from_numpy(init_noise(args.seed, t, sl.gt[t], 5.0, 5.0)).to(dev) for t in frames]
+        ol = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(4096, dtype=torch.float64, device=dev),
+                  n=torch.empty(4096, dtype=torch.int32, device=dev), trace=None)
+        voll.track(dl[0], sl.intr, tl[0], pst_l, sl.params, out=ol)
+        voll.integrate(dl[0], sl.intr, ol["T"])
+        torch.cuda.synchronize()
+        pft.profile_start()
+        ms = []
+        for f in range(1, len(frames)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            voll.track(dl[f], sl.intr, tl[f], pst_l, sl.params, out=ol)
+            voll.integrate(dl[f], sl.intr, ol["T"])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        pl = pft.profile_stop()
+        nvl = strided_valid(sl.depth(frames[1]), 4)
+        large = {"workload": "L: 1024^3 @5 mm fp16 V+W, tau 2 cm, K=4096, 10 iters, 640x480",
+                 "ms_per_frame_median": statistics.median(ms),
+                 "evals_per_s": 4096 * nvl * ITERS / (statistics.median(ms) * 1e-3),
+                 "kernel_ms_per_frame": {k: v[0] / len(ms) for k, v in pl.items() if v[1]}}
+        voll.close()
+        del pst_l, dl, tl, ol
+
     res = {
         "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
         "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -294,6 +334,7 @@ def run_ours(args):
                      "evals_per_s_kernel": evals_per_launch / avg_launch_s},
         "clocks": clk.summary(),
         "particle_sweep": sweep,
+        "large_volume": large,
         "pose_err_vs_gt": {"rot_deg_median": statistics.median(rot_err), "rot_deg_p90": float(np.percentile(rot_err, 90)),
                            "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),
                            "note": "paper-literal RO from GT (+) U+-5deg/+-5cm, per frame (SURVEY.md 8(c-5))"},

@@ -108,68 +108,105 @@ __global__ void k_depth_tiles(Intr K, double max_depth, const uint16_t* __restri
     }
   }
   for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
-  if (threadIdx.x == 0) tiles[t] = m;
+  if (threadIdx.x == 0) {
+    tiles[t] = m;
+    if (m) atomicMax(tiles + ntx * nty + (ty >> 3) * ((ntx + 7) >> 3) + (tx >> 3), m);  // coarse 64x64-px level
+  }
 }
 
-// One thread per brick.  A brick is dropped only when no voxel centre in it can pass the
-// voxel-level tests: all z_c <= 0, or its projection misses the image, or every pixel it can
-// project to is invalid / has d + tau <= z_c.  Bounds use the bounding sphere of the brick's
-// voxel centres with margins (1 mm, 2 px) far above fp32 rounding at room scale.
-__global__ void k_cull(Geom g, Intr K, const double* __restrict__ Tdev, const uint32_t* __restrict__ tiles,
-                       int ntx, int nty, uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
-  const uint32_t nb = (uint32_t)g.nbx * g.nby * g.nbz;
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false;
-  if (b < nb) {
-    const int bx = (int)(b % (uint32_t)g.nbx);
-    const uint32_t r = b / (uint32_t)g.nbx;
-    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
-    // centre of the brick's voxel-centre box and its radius
-    const float vox = (float)g.voxel;
-    const float cwx = (float)(g.ox + g.voxel * (4.0 * bx + 2.0)) - (float)Tdev[3];
-    const float cwy = (float)(g.oy + g.voxel * (4.0 * by + 2.0)) - (float)Tdev[7];
-    const float cwz = (float)(g.oz + g.voxel * (4.0 * bz + 2.0)) - (float)Tdev[11];
-    const float rad = 1.5f * 1.7320508f * vox + 1e-3f;
-    const float x = (float)Tdev[0] * cwx + (float)Tdev[4] * cwy + (float)Tdev[8] * cwz;
-    const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
-    const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
-    if (z + rad > 0.f) {
-      if (z - rad <= 1e-3f) {
-        keep = true;  // straddles the camera plane: no projection bound
-      } else {
-        const float zn = z - rad, zf = z + rad;
-        const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
-        const float u0 = fx * fminf((x - rad) / zn, (x - rad) / zf) + cx - 2.f;
-        const float u1 = fx * fmaxf((x + rad) / zn, (x + rad) / zf) + cx + 2.f;
-        const float v0 = fy * fminf((y - rad) / zn, (y - rad) / zf) + cy - 2.f;
-        const float v1 = fy * fmaxf((y + rad) / zn, (y + rad) / zf) + cy + 2.f;
-        if (u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H) {
-          const int pu0 = max(0, (int)floorf(u0 + 0.5f)), pu1 = min(K.W - 1, (int)floorf(u1 + 0.5f));
-          const int pv0 = max(0, (int)floorf(v0 + 0.5f)), pv1 = min(K.H - 1, (int)floorf(v1 + 0.5f));
-          const int t0x = pu0 / kTile, t1x = pu1 / kTile, t0y = pv0 / kTile, t1y = pv1 / kTile;
-          if ((t1x - t0x + 1) * (t1y - t0y + 1) > 64) {
-            keep = true;  // very close brick: do not bother bounding the depth
-          } else {
-            uint32_t m = 0;
-            for (int ty = t0y; ty <= t1y; ++ty)
-              for (int tx = t0x; tx <= t1x; ++tx) m = max(m, __ldg(tiles + ty * ntx + tx));
-            if (m > 0) {
-              const float dmax = (float)((double)m * K.unit);
-              keep = zn - 1e-3f < dmax + (float)g.trunc;
-            }
-          }
-        }
-      }
-    }
+// Conservative visibility test of a box of voxel centres given by its centre (world, fp64) and
+// bounding-sphere radius: false only when no voxel centre inside can pass the voxel-level tests
+// (all z_c <= 0, projection misses the image, or every pixel it can project to is invalid or has
+// d + tau <= z_c).  fp32 with margins (1 mm, 2 px) far above fp32 rounding at room scale.  Boxes
+// straddling the camera plane, or covering more than max_tiles depth tiles, are kept.
+__device__ __forceinline__ bool box_visible(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
+                                            const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
+                                            double czw, float rad, int max_tiles) {
+  const float cwx = (float)(cxw - Tdev[3]), cwy = (float)(cyw - Tdev[7]), cwz = (float)(czw - Tdev[11]);
+  const float x = (float)Tdev[0] * cwx + (float)Tdev[4] * cwy + (float)Tdev[8] * cwz;
+  const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
+  const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
+  if (!(z + rad > 0.f)) return false;
+  if (z - rad <= 1e-3f) return true;  // straddles the camera plane: no projection bound
+  const float zn = z - rad, zf = z + rad;
+  const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
+  const float u0 = fx * fminf((x - rad) / zn, (x - rad) / zf) + cx - 2.f;
+  const float u1 = fx * fmaxf((x + rad) / zn, (x + rad) / zf) + cx + 2.f;
+  const float v0 = fy * fminf((y - rad) / zn, (y - rad) / zf) + cy - 2.f;
+  const float v1 = fy * fmaxf((y + rad) / zn, (y + rad) / zf) + cy + 2.f;
+  if (!(u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H)) return false;
+  const int pu0 = max(0, (int)floorf(u0 + 0.5f)), pu1 = min(K.W - 1, (int)floorf(u1 + 0.5f));
+  const int pv0 = max(0, (int)floorf(v0 + 0.5f)), pv1 = min(K.H - 1, (int)floorf(v1 + 0.5f));
+  int t0x = pu0 / kTile, t1x = pu1 / kTile, t0y = pv0 / kTile, t1y = pv1 / kTile;
+  const uint32_t* lvl = tiles;
+  int stride = ntx;
+  if ((t1x - t0x + 1) * (t1y - t0y + 1) > 64) {  // large footprint: the coarse (8x8-tile) level
+    const int nty_f = (K.H + kTile - 1) / kTile;
+    lvl = tiles + ntx * nty_f;
+    stride = (ntx + 7) >> 3;
+    t0x >>= 3; t1x >>= 3; t0y >>= 3; t1y >>= 3;
+    if ((t1x - t0x + 1) * (t1y - t0y + 1) > max_tiles) return true;
   }
-  // warp-aggregated append
+  uint32_t m = 0;
+  for (int ty = t0y; ty <= t1y; ++ty)
+    for (int tx = t0x; tx <= t1x; ++tx) m = max(m, __ldg(lvl + ty * stride + tx));
+  if (m == 0) return false;
+  const float dmax = (float)((double)m * K.unit);
+  return zn - 1e-3f < dmax + (float)g.trunc;
+}
+
+__device__ __forceinline__ void append_warp(bool keep, uint32_t v, uint32_t* __restrict__ list,
+                                            uint32_t* __restrict__ count) {
   const unsigned ball = __ballot_sync(0xffffffffu, keep);
   if (ball) {
     const int lane = threadIdx.x & 31;
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(count, (uint32_t)__popc(ball));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) list[base + __popc(ball & ((1u << lane) - 1))] = b;
+    if (keep) list[base + __popc(ball & ((1u << lane) - 1))] = v;
+  }
+}
+
+constexpr int kSuper = 8;  // super-brick = 8^3 bricks = 32^3 voxels
+
+// Level 1: one thread per super-brick.
+__global__ void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev, const uint32_t* __restrict__ tiles,
+                             int ntx, int nsx, int nsy, int nsz, uint32_t* __restrict__ slist,
+                             uint32_t* __restrict__ scount) {
+  const uint32_t ns = (uint32_t)nsx * nsy * nsz;
+  const uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (sb < ns) {
+    const int sx = (int)(sb % (uint32_t)nsx);
+    const uint32_t r = sb / (uint32_t)nsx;
+    const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
+    // voxel-centre box of the super-brick: voxels [32 s, 32 s + 31] per axis
+    const double h = 16.0;
+    keep = box_visible(g, K, Tdev, tiles, ntx, g.ox + g.voxel * (32.0 * sx + h), g.oy + g.voxel * (32.0 * sy + h),
+                       g.oz + g.voxel * (32.0 * sz + h), (float)(15.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
+  }
+  append_warp(keep, sb, slist, scount);
+}
+
+// Level 2: the 512 bricks of every surviving super-brick (one CTA of 512 threads per super-brick).
+__global__ __launch_bounds__(512) void k_cull_bricks(Geom g, Intr K, const double* __restrict__ Tdev,
+                                                     const uint32_t* __restrict__ tiles, int ntx, int nsx, int nsy,
+                                                     const uint32_t* __restrict__ slist,
+                                                     const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
+                                                     uint32_t* __restrict__ count) {
+  const uint32_t n = *scount;
+  const int t = threadIdx.x;
+  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
+    const uint32_t sb = slist[li];
+    const int sx = (int)(sb % (uint32_t)nsx);
+    const uint32_t r = sb / (uint32_t)nsx;
+    const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
+    const int bx = sx * kSuper + (t & 7), by = sy * kSuper + ((t >> 3) & 7), bz = sz * kSuper + (t >> 6);
+    bool keep = false;
+    if (bx < g.nbx && by < g.nby && bz < g.nbz)
+      keep = box_visible(g, K, Tdev, tiles, ntx, g.ox + g.voxel * (4.0 * bx + 2.0), g.oy + g.voxel * (4.0 * by + 2.0),
+                         g.oz + g.voxel * (4.0 * bz + 2.0), (float)(1.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
+    append_warp(keep, ((uint32_t)bz * g.nby + (uint32_t)by) * g.nbx + (uint32_t)bx, list, count);
   }
 }
 
@@ -212,7 +249,8 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   Intr K{Kp->fx, Kp->fy, Kp->cx, Kp->cy, Kp->depth_unit_m, Kp->width, Kp->height};
   const Geom& g = vol->g;
   const int ntx = (K.W + kTile - 1) / kTile, nty = (K.H + kTile - 1) / kTile;
-  if ((size_t)ntx * nty * 4 > vol->L.tiles_bytes) full_sweep = 1;
+  const size_t ntiles_all = (size_t)ntx * nty + (size_t)((ntx + 7) >> 3) * ((nty + 7) >> 3);
+  if (ntiles_all * 4 > vol->L.tiles_bytes) full_sweep = 1;
   if (full_sweep) {
     size_t n = vol->L.elems;
     size_t blocks = (n + 255) / 256;
@@ -232,14 +270,19 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   uint32_t* dcount = (uint32_t*)(vol->base + vol->L.scratch_off + 128);
   uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
   uint32_t* dlist = (uint32_t*)(vol->base + vol->L.dlist_off);
-  cudaMemsetAsync(count, 0, 128, st);  // active count and dirty count
+  cudaMemsetAsync(count, 0, 192, st);  // active, dirty and super-brick counts (scratch +64..+255)
+  cudaMemsetAsync(tiles + (size_t)ntx * nty, 0, 4 * (size_t)((ntx + 7) >> 3) * ((nty + 7) >> 3), st);  // coarse level
   {
     dim3 blk(32, 8);
     int nt = ntx * nty;
     PFT_LAUNCH(PFT_PROF_CULL, st, k_depth_tiles<<<(nt + 7) / 8, blk, 0, st>>>(K, g.max_depth, depth, tiles, ntx, nty));
   }
-  const uint32_t nb = (uint32_t)g.nbx * g.nby * g.nbz;
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull<<<(nb + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nty, list, count));
+  const int nsx = (g.nbx + kSuper - 1) / kSuper, nsy = (g.nby + kSuper - 1) / kSuper, nsz = (g.nbz + kSuper - 1) / kSuper;
+  const uint32_t ns = (uint32_t)nsx * nsy * nsz;
+  uint32_t* slist = (uint32_t*)(vol->base + vol->L.slist_off);
+  uint32_t* scount = (uint32_t*)(vol->base + vol->L.scratch_off + 192);
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, nsz, slist, scount));
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<148 * 4, 512, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, slist, scount, list, count));
   const int grid = 148 * 8;
   if (vol->esize == 4)
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (float*)(vol->base + vol->L.v_off),

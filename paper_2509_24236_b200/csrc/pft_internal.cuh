@@ -46,6 +46,7 @@ struct VolLayout {
   size_t m_off;                       // in-band mask: one uint64 per brick, bit w = cell w
   size_t list_off, list_bytes;        // integration: active brick list (uint32 per brick)
   size_t dirty_off, dlist_off;        // records: dirty flag per cell-brick + dirty list (uint32 each)
+  size_t slist_off;                   // integration: surviving super-bricks (8^3 bricks) list
   size_t tiles_off, tiles_bytes;      // integration: per-tile depth max (float)
   size_t total;
 };

@@ -50,6 +50,7 @@ static pft_status make_layout(const pft_volume_desc* d, Geom* g, VolLayout* L, s
   L->m_off = off; off = align_up(off + nb * 8, 256);
   L->list_off = off; L->list_bytes = nb * 4; off = align_up(off + L->list_bytes, 256);
   L->dirty_off = off; off = align_up(off + nb * 4, 256);
+  L->slist_off = off; off = align_up(off + ((nb + 511) / 512 + 64) * 4 * 8, 256);  // super-brick list
   L->dlist_off = off; off = align_up(off + nb * 4, 256);
   L->tiles_off = off; L->tiles_bytes = 64 * 1024 * 4; off = align_up(off + L->tiles_bytes, 256);
   L->total = off;
