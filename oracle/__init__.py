@@ -79,6 +79,8 @@ def lib():
         _lib.ora_integrate.argtypes = [P, P, P, P, P, P, C.c_int32]
         _lib.ora_reset.restype = None
         _lib.ora_reset.argtypes = [P, P, P]
+        _lib.ora_extract.restype = C.c_int64
+        _lib.ora_extract.argtypes = [P, P, P, P, C.c_int64]
         _lib.ora_round_to_storage.restype = C.c_double
         _lib.ora_round_to_storage.argtypes = [C.c_double, C.c_int32]
     return _lib
@@ -192,6 +194,13 @@ class OracleVolume:
                             C.byref(cp), _p(ws), _p(T), _p(E), _p(n), _p(tr), _p(m),
                             nthreads or default_threads())
         return dict(T=T.reshape(3, 4), E=E, n=n, trace=tr, N=N, margin=float(m[0]))
+
+    def extract(self, max_pts=None):
+        """F4 zero-crossing surface points (N x 3, canonical voxel/axis order)."""
+        n = lib().ora_extract(_p(self.V), _p(self.W), C.byref(self.cdesc), None, 0)
+        pts = np.zeros((max(n, 1), 3))
+        lib().ora_extract(_p(self.V), _p(self.W), C.byref(self.cdesc), _p(pts), n)
+        return pts[:n]
 
     def eval_poses(self, depth, intr, poses, stride, rho=0.0, nthreads=None):
         depth = np.ascontiguousarray(depth, dtype=np.uint16)

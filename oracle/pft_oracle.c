@@ -458,3 +458,44 @@ void ora_reset(void *V, void *Wt, const ora_volume_desc *D) {
     store_val(Wt, D->storage, i, 0.0);
   }
 }
+
+/* ------------------------------------------------------------------ F4: surface points */
+/* Zero-crossing surface points of the TSDF (NEXT F4; SPEC.md:255-262 extract_surface_points,
+ * feeding the completeness / accuracy metrics of PAPER.md:562-563).  For every voxel (i,j,k),
+ * x fastest, and each axis a = x, y, z in that order whose +1 neighbour is inside the grid: if
+ * both voxels are observed (W > 0) and (V0 > 0) != (V1 > 0) with not both zero, emit
+ *   t = V0 / (V0 - V1),  p = c0 + (t * s) e_a,   c0 = o + s (i + 1/2, j + 1/2, k + 1/2).
+ * Writes up to max_pts points (x, y, z) and returns the total number of crossings. */
+int64_t ora_extract(const void *V, const void *Wt, const ora_volume_desc *D, double *pts, int64_t max_pts) {
+  int64_t n = 0;
+  const int32_t dims[3] = {D->nx, D->ny, D->nz};
+  for (int32_t k = 0; k < D->nz; ++k)
+    for (int32_t j = 0; j < D->ny; ++j)
+      for (int32_t i = 0; i < D->nx; ++i) {
+        size_t idx = ((size_t)k * D->ny + (size_t)j) * D->nx + (size_t)i;
+        double w0 = load_val(Wt, D->storage, idx);
+        if (!(w0 > 0.0)) continue;
+        double v0 = load_val(V, D->storage, idx);
+        int32_t c[3] = {i, j, k};
+        for (int a = 0; a < 3; ++a) {
+          if (c[a] + 1 >= dims[a]) continue;
+          size_t step = a == 0 ? 1 : (a == 1 ? (size_t)D->nx : (size_t)D->nx * D->ny);
+          double w1 = load_val(Wt, D->storage, idx + step);
+          if (!(w1 > 0.0)) continue;
+          double v1 = load_val(V, D->storage, idx + step);
+          if ((v0 > 0.0) == (v1 > 0.0) || (v0 == 0.0 && v1 == 0.0)) continue;
+          double t = v0 / (v0 - v1);
+          if (n < max_pts) {
+            double p[3] = {D->origin_m[0] + D->voxel_m * ((double)i + 0.5),
+                           D->origin_m[1] + D->voxel_m * ((double)j + 0.5),
+                           D->origin_m[2] + D->voxel_m * ((double)k + 0.5)};
+            p[a] = p[a] + t * D->voxel_m;
+            pts[3 * n + 0] = p[0];
+            pts[3 * n + 1] = p[1];
+            pts[3 * n + 2] = p[2];
+          }
+          n++;
+        }
+      }
+  return n;
+}

@@ -150,3 +150,67 @@ def test_paper_schedule_runs_and_converges_on_tiny():
     assert np.all(np.diff(tr[ran, 2]) <= 0)
     assert list(tr[:3, 22]) == [10240, 3072, 1024]
     assert int(tr[ran][-1, 19]) & 16 or ran.sum() == 20
+
+
+# ------------------------------------------------------------------ F4 surface points
+def test_extract_fresh_volume_is_empty():
+    """a fresh (unobserved) volume has no surface points."""
+    from synth.configs import VolumeDesc
+    vol = oracle.OracleVolume(VolumeDesc(12, 10, 8, 0.1, (0.0, 0.0, 0.0), 0.3))
+    assert len(vol.extract()) == 0
+
+
+def test_extract_plane_closed_form():
+    """A linear field V = (z - z0)/tau (analytic fill, W = 1) crosses zero exactly at z0: every
+    extracted point lies on z = z0 (up to the fp32 rounding of the stored values), only z-edges
+    cross, and there is one crossing per (i, j) column."""
+    from synth.configs import VolumeDesc
+    n, s, tau, z0 = 16, 0.1, 0.3, 0.83
+    desc = VolumeDesc(n, n, n, s, (0.0, 0.0, 0.0), tau)
+    z = (np.arange(n) + 0.5) * s
+    col = np.clip((z - z0) / tau, -1, 1).astype(np.float32)
+    V = np.broadcast_to(col[:, None, None], (n, n, n)).astype(np.float32).ravel()
+    W = np.ones_like(V)
+    pts = oracle.OracleVolume(desc, V, W).extract()
+    assert len(pts) == n * n
+    assert np.abs(pts[:, 2] - z0).max() < 1e-6
+    xs = np.sort(np.unique(np.round(pts[:, 0], 9)))
+    assert np.allclose(xs, (np.arange(n) + 0.5) * s)
+
+
+def test_extract_sphere_radii():
+    """SPEC.md:262 analytic sphere (config T fill): extracted points lie within one voxel of the
+    sphere or the ground plane."""
+    c = config_tiny(seed=1)
+    pts = oracle.OracleVolume(c["desc"], c["V"], c["W"]).extract()
+    assert len(pts) > 1000
+    d = np.abs(c["scene"].sdf(pts))
+    assert d.max() < c["desc"].voxel_m and np.sqrt(np.mean(d ** 2)) < c["desc"].voxel_m / 2
+
+
+def test_extract_ignores_unobserved_and_brute_force_small():
+    """Brute force on a random 5x4x3 grid with unobserved voxels: the oracle's list equals a direct
+    enumeration of the definition (edges between observed voxels with a sign change)."""
+    from synth.configs import VolumeDesc
+    rng = np.random.default_rng(3)
+    nx, ny, nz, s = 5, 4, 3, 0.1
+    desc = VolumeDesc(nx, ny, nz, s, (0.1, -0.2, 0.3), 0.3)
+    V = rng.choice([-0.75, -0.25, 0.0, 0.5, 1.0], size=nx * ny * nz).astype(np.float32)
+    W = rng.choice([0.0, 1.0, 2.0], size=nx * ny * nz).astype(np.float32)
+    got = oracle.OracleVolume(desc, V, W).extract()
+    Vg, Wg = V.reshape(nz, ny, nx).astype(float), W.reshape(nz, ny, nx)
+    exp = []
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                for a, (di, dj, dk) in enumerate([(1, 0, 0), (0, 1, 0), (0, 0, 1)]):
+                    i1, j1, k1 = i + di, j + dj, k + dk
+                    if i1 >= nx or j1 >= ny or k1 >= nz or Wg[k, j, i] <= 0 or Wg[k1, j1, i1] <= 0:
+                        continue
+                    v0, v1 = Vg[k, j, i], Vg[k1, j1, i1]
+                    if (v0 > 0) == (v1 > 0) or (v0 == 0 and v1 == 0):
+                        continue
+                    p = [0.1 + s * (i + 0.5), -0.2 + s * (j + 0.5), 0.3 + s * (k + 0.5)]
+                    p[a] = p[a] + (v0 / (v0 - v1)) * s
+                    exp.append(p)
+    assert np.array_equal(got, np.array(exp).reshape(-1, 3))
