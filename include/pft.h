@@ -164,6 +164,15 @@ pft_status pft_integrate(pft_volume* vol, const uint16_t* dev_depth, const pft_i
 pft_status pft_integrate_ex(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K,
                             const double* dev_T, int32_t flags, void* stream);
 
+/* NEXT F4: zero-crossing surface points, input of the completeness / accuracy
+ * metrics of PAPER.md:562-563.  For every voxel and axis whose +1 neighbour is in the grid, both
+ * observed (W > 0), values of different sign (not both 0): t = V0/(V0 - V1), point = voxel centre
+ * + t * voxel along the axis (fp64, bit-identical to a plain evaluation).  dev_points: max_points x 3
+ * doubles (world, metres), unordered; *dev_count (device int64) = total crossings (may exceed
+ * max_points: only the first max_points are written; call with max_points = 0 to size). */
+pft_status pft_extract_surface(const pft_volume* vol, double* dev_points, int64_t max_points,
+                               int64_t* dev_count, void* stream);
+
 /* ---------------------------------------------------------------- tracking */
 
 /* Workspace bytes pft_track / pft_eval_poses need for this frame geometry and K particles

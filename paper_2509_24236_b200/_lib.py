@@ -17,7 +17,7 @@ STATUS = {0: "PFT_OK", -1: "PFT_ERR_INVALID_ARG", -2: "PFT_ERR_BUFFER_TOO_SMALL"
 
 # every symbol include/pft.h declares (checked by tests/test_abi.py)
 EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_volume_upload", "pft_volume_download",
-           "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex",
+           "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_extract_surface",
            "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
            "pft_comm_init", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
@@ -72,6 +72,7 @@ def lib():
         "pft_volume_destroy": [P],
         "pft_integrate": [P, P, P, P, P],
         "pft_integrate_ex": [P, P, P, P, I32, P],
+        "pft_extract_surface": [P, P, C.c_int64, P, P],
         "pft_track_workspace_bytes": [P, P, I32, P, P],
         "pft_track": [P, P, P, P, P, I32, P, P, SZ, P, P, P, P, P],
         "pft_eval_poses": [P, P, P, P, P, I32, P, SZ, P, P, P],

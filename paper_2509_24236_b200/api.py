@@ -113,6 +113,17 @@ class Volume:
         check(lib().pft_integrate_ex(self.handle, _vp(depth), C.byref(ci), _vp(T),
                                      INTEGRATE_FULL_SWEEP if full_sweep else 0, _stream(stream)))
 
+    def extract_surface(self, max_points=None, stream=None):
+        """F4 zero-crossing surface points -> (N, 3) fp64 device tensor (unordered)."""
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        if max_points is None:
+            check(lib().pft_extract_surface(self.handle, C.c_void_p(0), 0, _vp(cnt), _stream(stream)))
+            max_points = int(cnt.item())
+        pts = torch.empty(max(max_points, 1), 3, dtype=torch.float64, device=self.device)
+        check(lib().pft_extract_surface(self.handle, _vp(pts), int(max_points), _vp(cnt), _stream(stream)))
+        n = int(cnt.item())
+        return pts[:min(n, max_points)]
+
     # --------------------------------------------------------------- tracking
     def workspace(self, intr, nparticles, params):
         ci, cp = make_intr(intr), make_params(params)

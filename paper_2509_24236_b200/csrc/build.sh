@@ -8,6 +8,6 @@ EXTRA="$@"
 NCCL_INC=$(python -c 'import nvidia.nccl, os; print(os.path.join(list(nvidia.nccl.__path__)[0], "include"))')
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
   -Xptxas -v $EXTRA -I"$NCCL_INC" \
-  "$HERE/volume.cu" "$HERE/integrate.cu" "$HERE/track.cu" "$HERE/abi.cu" \
+  "$HERE/volume.cu" "$HERE/integrate.cu" "$HERE/track.cu" "$HERE/extract.cu" "$HERE/abi.cu" \
   -o "$OUT.tmp" -ldl 2> "$HERE/../ptxas.log" || { cat "$HERE/../ptxas.log"; exit 1; }
 mv "$OUT.tmp" "$OUT"

@@ -375,3 +375,41 @@ def test_track_stop_rules(pft, stop):
     assert np.all(r["trace"][~ran] == o["trace"][~ran])
     assert_pose_close(r["T"], o["T"], stop)
     vol.close()
+
+
+# ------------------------------------------------------------------ NEXT row F4
+def _sorted_rows(p):
+    p = np.asarray(p)
+    return p[np.lexsort((p[:, 2], p[:, 1], p[:, 0]))] if len(p) else p.reshape(0, 3)
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_extract_surface_bit_exact(pft, storage):
+    """F4 zero-crossing points of a fused room volume (and of config T's analytic fill): the GPU's
+    unordered list equals the oracle's, sorted, bit for bit; a fresh volume yields none."""
+    from synth.configs import room_gt_pose
+    scene = box_room(seed=5)
+    desc = VolumeDesc(96, 96, 96, 0.03, (-1.44, -1.44, -1.44), 0.09, storage=storage)
+    intr = Intrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    T0 = room_gt_pose(scene, 5)
+    vol = gpu_volume(pft, desc)
+    assert len(vol.extract_surface()) == 0
+    ov = oracle.OracleVolume(desc)
+    for f in range(3):
+        Tf = perturb(T0, [0.0, 0.0, 0.15 * f], [0.0, 0.04 * f, 0.0], 10.0, 10.0)
+        depth = render_depth(scene, intr, Tf, Stream(5, 4_000_000 + f))
+        vol.integrate(T(depth), intr, T(Tf))
+        ov.integrate(depth, intr, Tf)
+    g = vol.extract_surface().cpu().numpy()
+    o = ov.extract()
+    assert len(o) > 2000 and len(g) == len(o)
+    assert np.array_equal(_sorted_rows(g), _sorted_rows(o))
+    # truncated output: the count still reports every crossing
+    cnt_only = vol.extract_surface(max_points=100)
+    assert len(cnt_only) == 100
+    vol.close()
+    c = config_tiny(seed=1)
+    vt = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    assert np.array_equal(_sorted_rows(vt.extract_surface().cpu().numpy()),
+                          _sorted_rows(oracle.OracleVolume(c["desc"], c["V"], c["W"]).extract()))
+    vt.close()
