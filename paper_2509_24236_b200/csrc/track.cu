@@ -824,7 +824,7 @@ struct PArgs {
   BPFrame f;
   Sched sc;
   const float* pst;
-  int K, conv, iters, rule, guard, sched;
+  int K, conv, iters, rule, guard, sched, tail_pct;
   double beta, rho, omega0, v0;
   StopRule sr;
   const double* T_init;
@@ -839,6 +839,7 @@ struct PArgs {
   double* upart;
   unsigned long long* cpart;
   unsigned* work;
+  unsigned long long* tdone;   // PFT_PHASE_TIMING: per-CTA P2 finish times (nullptr: off)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -893,6 +894,23 @@ __device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsi
   }
 }
 
+// Sum of the G per-CTA centre partials (S, n), read by all threads (2 loads each) and reduced by
+// warp shuffles + smem: the same exact integers in every CTA, ~L2 latency instead of G of them.
+__device__ __forceinline__ void sum_partials(const unsigned long long* cp, int G, unsigned long long* sS,
+                                             unsigned* sN, unsigned long long& S, unsigned long long& n) {
+  unsigned long long s = 0ull, c = 0ull;
+  for (int b = threadIdx.x; b < G; b += kThreads) { s += __ldcg(cp + 2 * b); c += __ldcg(cp + 2 * b + 1); }
+  for (int sft = 16; sft > 0; sft >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, sft);
+    c += __shfl_xor_sync(0xffffffffu, c, sft);
+  }
+  if ((threadIdx.x & 31) == 0) { sS[threadIdx.x >> 5] = s; sN[threadIdx.x >> 5] = (unsigned)c; }
+  __syncthreads();
+  S = 0ull; n = 0ull;
+  for (int w = 0; w < kThreads / 32; ++w) { S += sS[w]; n += sN[w]; }
+  __syncthreads();
+}
+
 // CTA total of the centre's (sum, cnt) -> thread 0.
 __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt, unsigned long long* sS, unsigned* sN,
                                             unsigned long long& S, unsigned& n) {
@@ -932,6 +950,10 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   TrackState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned gen = 0u;
+  // PFT_PHASE_TIMING accumulators (CTA 0, thread 0): B, P1, P2, P3, P4, P5, P2 tail, P0
+  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tmark = 0;
+  const bool timing = a.tdone != nullptr;
+  if (timing && tid == 0) tmark = global_ns();
   if (tid == 0) {
     gen = *(volatile unsigned*)&st->bar_gen;
 #pragma unroll
@@ -972,6 +994,13 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     sStalls = 0; sStop = 0; sSet = -1; sKlast = 0; sNc = 0u; sNA = 0;
   }
   grid_barrier(st, gen);
+#define PFT_TMARK(slot)                                        \
+  if (timing && tid == 0) {                                    \
+    const unsigned long long now_ = global_ns();               \
+    tph[slot] += now_ - tmark;                                 \
+    tmark = now_;                                              \
+  }
+  PFT_TMARK(7);
   const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
   int it = 0;
   for (; it < a.iters; ++it) {
@@ -993,15 +1022,16 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       // half 0 of the centre partials: P5 of the previous iteration may still be reading half 1
       if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
       grid_barrier(st, gen);
+      unsigned long long S2, n2;
+      sum_partials(a.cpart, gridDim.x, sS, sNw, S2, n2);
       if (tid == 0) {
-        unsigned long long S2 = 0ull, n2 = 0ull;
-        for (int b = 0; b < (int)gridDim.x; ++b) { S2 += __ldcg(a.cpart + 2 * b); n2 += __ldcg(a.cpart + 2 * b + 1); }
         sState[2] = fitness_c(S2, (unsigned)n2, a.rho, N);
         sNc = (unsigned)n2;
         sSet = set;
       }
       __syncthreads();
     }
+    PFT_TMARK(0);
     // ---- P1: candidate-pose table (K_i rows)
     for (int k = blockIdx.x * kThreads + tid; k < Ki; k += gridDim.x * kThreads) {
       double m[12];
@@ -1011,13 +1041,22 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
     }
     grid_barrier(st, gen);
+    PFT_TMARK(1);
     // ---- P2: particle x point evaluation, warp-granular items (group-major: item = group * nchunks
     // + chunk).  sched 0: one global dynamic queue; sched 1: CTA c owns the contiguous range
     // [c*n/G, (c+1)*n/G) (its warps share one image region -> L1 reuse), handed out by a CTA counter.
     {
+      // Items: the first ~80% of the particle chunks as 16-particle items, the rest as 4-particle
+      // items handed out last, so the queue drains on small items (short cross-CTA tail).
       const int ngroups = (pts.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
-      const int nchunks = (Ki + kItemParticles - 1) / kItemParticles;
-      const int nitems = ngroups * nchunks;
+      const int nch16 = (Ki + kItemParticles - 1) / kItemParticles;
+      // (only when there are few items per warp: with many, the tail is already negligible)
+      const bool few = (long long)ngroups * nch16 < 64LL * gridDim.x * (kThreads / 32);
+      const int cb = (a.sched == 1 || !few) ? nch16 : nch16 - (nch16 * a.tail_pct + 99) / 100;  // big chunks
+      const int ksmall = cb * kItemParticles;                           // first particle of the small part
+      const int nch4 = (Ki - ksmall + 3) / 4;
+      const int nbig = ngroups * cb;
+      const int nitems = nbig + ngroups * nch4;
       const int r0 = (int)((long long)nitems * blockIdx.x / gridDim.x);
       const int r1 = (int)((long long)nitems * (blockIdx.x + 1) / gridDim.x);
       if (tid == 0) sItem = 0;
@@ -1027,7 +1066,19 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(a.work + it, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (a.sched == 1 ? r1 : nitems)) break;
-        const int group = item / nchunks, chunk = item - group * nchunks;
+        int group, k0, k1;
+        if (item < nbig) {
+          group = item / cb;
+          const int chunk = item - group * cb;
+          k0 = chunk * kItemParticles;
+          k1 = min(Ki, k0 + kItemParticles);
+        } else {
+          const int it2 = item - nbig;
+          group = it2 / nch4;
+          const int chunk = it2 - group * nch4;
+          k0 = ksmall + chunk * 4;
+          k1 = min(Ki, k0 + 4);
+        }
         double px[kItemTiles], py[kItemTiles], pz[kItemTiles];
 #pragma unroll
         for (int p = 0; p < kItemTiles; ++p) {
@@ -1035,7 +1086,6 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
           px[p] = py[p] = pz[p] = 0.0;
           if (i < pts.npad) { px[p] = __ldcg(pts.x + i); py[p] = __ldcg(pts.y + i); pz[p] = __ldcg(pts.z + i); }
         }
-        const int k0 = chunk * kItemParticles, k1 = min(Ki, k0 + kItemParticles);
         // stage the item's poses in this warp's shared slot (6 x 16 B per pose, 3 per lane)
         double2* wp = sWPose[tid >> 5];
         int* wf = sWFlag[tid >> 5];
@@ -1079,7 +1129,21 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         __syncwarp();
       }
     }
+    if (timing) {
+      __syncthreads();
+      if (tid == 0) a.tdone[blockIdx.x] = global_ns();
+    }
     grid_barrier(st, gen);
+    if (timing && tid == 0 && blockIdx.x == 0) {
+      unsigned long long lo = ~0ull, hi = 0ull;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        const unsigned long long v = __ldcg(a.tdone + b);
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+      }
+      tph[6] += hi - lo;
+    }
+    PFT_TMARK(2);
     // ---- P3: E_k, advantage set, per-block partials (same tree as k_update)
     const double Ebase = sState[2];
     const int nblk = (Ki + 255) / 256;
@@ -1105,6 +1169,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       __syncthreads();
     }
     grid_barrier(st, gen);
+    PFT_TMARK(3);
     // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
 #pragma unroll
     for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
@@ -1140,15 +1205,16 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       if (tid == 0) { cp1[2 * blockIdx.x] = S; cp1[2 * blockIdx.x + 1] = n; }
       grid_barrier(st, gen);  // sNA is identical in every CTA: uniform barrier
     }
+    PFT_TMARK(4);
     // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
+    unsigned long long S5 = 0ull, n5 = 0ull;
+    if (sNA > 0) sum_partials(a.cpart + 2 * (size_t)gridDim.x, gridDim.x, sS, sNw, S5, n5);
     if (tid == 0) {
       double Ec = sState[3];
       unsigned nc = sNcBase;
       int rejected = 0;
       if (sNA > 0) {
-        const unsigned long long* cp1 = a.cpart + 2 * (size_t)gridDim.x;
-        unsigned long long S = 0ull, n = 0ull;
-        for (int b = 0; b < (int)gridDim.x; ++b) { S += __ldcg(cp1 + 2 * b); n += __ldcg(cp1 + 2 * b + 1); }
+        const unsigned long long S = S5, n = n5;
         const double En = fitness_c(S, (unsigned)n, a.rho, N);
         if (a.guard && En > sState[3]) {  // F3 guard: keep P^(i-1)
           rejected = 1;
@@ -1173,8 +1239,14 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       sKlast = Ki; sRej = rejected;
     }
     __syncthreads();
+    PFT_TMARK(5);
     if (sStop) { ++it; break; }  // identical decision in every CTA
   }
+  if (timing && tid == 0 && blockIdx.x == 0)
+    printf("pft phase timing (us, %d iterations, %d CTAs): P0 %.1f  B %.1f  P1 %.1f  P2 %.1f (tail %.1f)  P3 %.1f  P4 %.1f  P5 %.1f\n",
+           it, (int)gridDim.x, tph[7] * 1e-3, tph[0] * 1e-3, tph[1] * 1e-3, tph[2] * 1e-3, tph[6] * 1e-3,
+           tph[3] * 1e-3, tph[4] * 1e-3, tph[5] * 1e-3);
+#undef PFT_TMARK
   // ---- outputs
   if (blockIdx.x == 0 && tid == 0) {
     for (int q = 0; q < 12; ++q) { a.T_out[q] = sP[q]; st->P[q] = sP[q]; }
@@ -1242,7 +1314,7 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   L->part_off = off; off = align_up(off + kUpdW * sizeof(double) * (size_t)L->nblk_upd, 256);
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
   L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
-  L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024, 256);
+  L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024 + sizeof(unsigned long long) * 148 * 8, 256);
   L->total = off;
   return PFT_OK;
 }
@@ -1345,6 +1417,8 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.K = Kp; pa.conv = prm->delta_conv; pa.iters = prm->iters; pa.rule = prm->update_rule; pa.guard = prm->guard;
   static const int sched = [] { const char* e = getenv("PFT_EVAL_SCHED"); return e ? atoi(e) : 0; }();
   pa.sched = sched;
+  static const int tail_pct = [] { const char* e = getenv("PFT_TAIL_PCT"); return e ? atoi(e) : 5; }();
+  pa.tail_pct = tail_pct;
   pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
   pa.sr = StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit};
   pa.T_init = T_init;
@@ -1356,6 +1430,8 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.upart = (double*)(c.ws + c.L.part_off);
   pa.cpart = (unsigned long long*)(c.ws + c.L.cpart_off);
   pa.work = (unsigned*)(c.ws + c.L.work_off);
+  static const bool timing = [] { const char* e = getenv("PFT_PHASE_TIMING"); return e && e[0] == '1'; }();
+  pa.tdone = timing ? (unsigned long long*)(c.ws + c.L.work_off + 1024 * sizeof(unsigned)) : nullptr;
   void* args[] = {&pa};
   cudaError_t e = cudaSuccess;
   PFT_LAUNCH(PFT_PROF_TRACK, c.st,
