@@ -256,6 +256,12 @@ uint64_t pft_launch_count(void);
 pft_status pft_profile_start(void);
 pft_status pft_profile_stop(double* ms_out, int64_t* launches_out);
 
+/* Test/debug: emulate nranks particle shards on this one GPU (SURVEY.md §4 "virtual shards"):
+ * pft_track then runs the multi-GPU code path with rank r's evaluation launched in turn and the
+ * all-gather replaced by device copies; results must equal the 1-rank run bit for bit.  Not for
+ * production (the shards run sequentially). */
+pft_status pft_comm_init_virtual(pft_volume* vol, int32_t nranks);
+
 /* Thread-local message describing the last non-OK status of this thread. */
 const char* pft_last_error(void);
 

@@ -19,7 +19,7 @@ STATUS = {0: "PFT_OK", -1: "PFT_ERR_INVALID_ARG", -2: "PFT_ERR_BUFFER_TOO_SMALL"
 EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_volume_upload", "pft_volume_download",
            "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_extract_surface",
            "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
-           "pft_comm_init", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
+           "pft_comm_init", "pft_comm_init_virtual", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
 PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records", "track"]
 
@@ -79,6 +79,7 @@ def lib():
         "pft_track_info": [P, P, P],
         "pft_comm_get_unique_id": [P],
         "pft_comm_init": [P, P, I32, I32],
+        "pft_comm_init_virtual": [P, I32],
         "pft_profile_start": [],
         "pft_profile_stop": [P, P],
     }

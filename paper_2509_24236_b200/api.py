@@ -188,6 +188,12 @@ class Volume:
         self.nranks, self.rank = world, rank
         self._ws = {}
 
+    def comm_init_virtual(self, nranks):
+        """Test/debug: run the multi-GPU path with nranks sequential shards on this GPU."""
+        check(lib().pft_comm_init_virtual(self.handle, int(nranks)))
+        self.nranks, self.rank = int(nranks), 0
+        self._ws = {}
+
     def close(self):
         if getattr(self, "handle", None):
             lib().pft_volume_destroy(self.handle)

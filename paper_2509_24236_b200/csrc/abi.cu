@@ -196,6 +196,16 @@ pft_status pft_comm_get_unique_id(uint8_t id_out[128]) {
   return PFT_OK;
 }
 
+pft_status pft_comm_init_virtual(pft_volume* vol, int32_t nranks) {
+  if (!vol) return fail(PFT_ERR_INVALID_ARG, "vol is NULL");
+  if (nranks < 1) return fail(PFT_ERR_INVALID_ARG, "nranks must be >= 1");
+  if (vol->nccl_comm) return fail(PFT_ERR_STATE, "a real communicator is attached");
+  vol->nranks = nranks;
+  vol->rank = 0;
+  vol->virtual_ranks = nranks > 1 ? nranks : 0;
+  return PFT_OK;
+}
+
 pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks, int32_t rank) {
   if (!vol || !id) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PFT_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);

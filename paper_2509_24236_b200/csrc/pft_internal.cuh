@@ -63,6 +63,7 @@ struct pft_volume {
   // multi-GPU
   void* nccl_comm;
   int nranks, rank;
+  int virtual_ranks;  // > 1: pft_comm_init_virtual (sequential shards, no NCCL)
 };
 
 namespace pft {

@@ -1466,11 +1466,21 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
     const int Ki = c.L.sched_K[j], set = c.L.sched_set[j];
     if (set != prev_set) launch_centre<T>(c, 0, set, it, Ki, prm, trace);  // baseline on the new set (L11)
     prev_set = set;
-    const int k_count = max(0, min(Ki, k_begin + kloc) - k_begin);
-    launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local, set);
-    if (G > 1) {
-      pft_status s = comm_allgather(c.vol, local, full, sizeof(PartRec) * (size_t)kloc, c.st);
-      if (s != PFT_OK) return s;
+    if (c.vol->virtual_ranks > 1) {
+      // virtual shards: rank q's evaluation, then its all-gather slot filled by a device copy
+      for (int q = 0; q < G; ++q) {
+        const int kb = q * kloc, kc = max(0, min(Ki, kb + kloc) - kb);
+        launch_eval<T>(c, 0, pst, kb, kc, prm->delta_conv, nullptr, local, set);
+        cudaMemcpyAsync(full + kb, local, sizeof(PartRec) * (size_t)kloc, cudaMemcpyDeviceToDevice, c.st);
+        cudaMemsetAsync(local, 0, sizeof(PartRec) * (size_t)kloc, c.st);
+      }
+    } else {
+      const int k_count = max(0, min(Ki, k_begin + kloc) - k_begin);
+      launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local, set);
+      if (G > 1) {
+        pft_status s = comm_allgather(c.vol, local, full, sizeof(PartRec) * (size_t)kloc, c.st);
+        if (s != PFT_OK) return s;
+      }
     }
     UpdArgs ua{c.state(), full, local, Ki, k_begin, kloc, pst, prm->delta_conv, prm->update_rule, set,
                prm->min_inband_frac, E, n_out, (double*)(c.ws + c.L.part_off)};

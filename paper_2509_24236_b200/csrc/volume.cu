@@ -287,7 +287,7 @@ pft_status pft_volume_create(const pft_volume_desc* desc, void* dev_storage, siz
   if (!v) return fail(PFT_ERR_INVALID_ARG, "host allocation failed");
   v->desc = *desc; v->g = g; v->L = L; v->esize = es; v->base = (char*)dev_storage;
   cudaGetDevice(&v->device);
-  v->nccl_comm = nullptr; v->nranks = 1; v->rank = 0;
+  v->nccl_comm = nullptr; v->nranks = 1; v->rank = 0; v->virtual_ranks = 0;
   *out = v;
   return PFT_OK;
 }
