@@ -51,8 +51,8 @@ typedef struct {
   int32_t iters, stride;
   double min_inband_frac;
   int32_t delta_conv;  /* 0 camera-centred (L10 default), 1 world-literal */
-  int32_t update_rule; /* 0 plain mean (paper, L14); 1 weighted by E_base - E_k (NEXT F3) */
-  int32_t topk;
+  int32_t update_rule; /* 0 plain mean (paper, L14); 1 weighted by E_base - E_k; 2 top-k (NEXT F3) */
+  int32_t topk;        /* rule 2: average the topk best members (smallest E_k, ties by lower k) */
   /* NEXT F1, the paper's schedule: iteration i uses the first sched_K[i % nsched]
    * template rows and the point set of strides (sched_sx, sched_sy); nsched = 0: (all, stride). */
   int32_t nsched;
@@ -324,8 +324,36 @@ int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth
     if (min_margin && margin < *min_margin) *min_margin = margin;
     double Q[4] = {0, 0, 0, 0}, U[3] = {0, 0, 0}, Wsum = 0.0;
     int32_t nA = 0;
+    /* F3 top-k: keep only the topk best members (smallest E_k, ties by lower k); they are then
+     * averaged with the plain mean in ascending k order and |A| reports their number. */
+    double Ecut = Ebase;
+    int32_t kcut = Ki;
+    if (prm->update_rule == 2) {
+      int32_t nmem = 0;
+      for (int32_t k = 0; k < Ki; ++k) nmem += E_out[k] < Ebase;
+      if (nmem > prm->topk) {
+        /* the topk-th smallest (E, k) pair: selection by repeated minimum (plain, O(topk K)) */
+        double pe = -1.0;
+        int32_t pk = -1;
+        for (int32_t r = 0; r < prm->topk; ++r) {
+          double be = 2.0;
+          int32_t bk = Ki;
+          for (int32_t k = 0; k < Ki; ++k) {
+            double e = E_out[k];
+            if (!(e < Ebase)) continue;
+            if (e < pe || (e == pe && k <= pk)) continue;        /* already taken */
+            if (e < be || (e == be && k < bk)) { be = e; bk = k; }
+          }
+          pe = be;
+          pk = bk;
+        }
+        Ecut = pe;
+        kcut = pk;
+      }
+    }
     for (int32_t k = 0; k < Ki; ++k) {
       if (E_out[k] < Ebase) {
+        if (prm->update_rule == 2 && kcut < Ki && (E_out[k] > Ecut || (E_out[k] == Ecut && k > kcut))) continue;
         double w = prm->update_rule == 1 ? Ebase - E_out[k] : 1.0;
         for (int j = 0; j < 4; ++j) Q[j] += w * q_all[4 * (size_t)k + j];
         for (int j = 0; j < 3; ++j) U[j] += w * u_all[3 * (size_t)k + j];

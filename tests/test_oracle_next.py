@@ -214,3 +214,32 @@ def test_extract_ignores_unobserved_and_brute_force_small():
                     p[a] = p[a] + (v0 / (v0 - v1)) * s
                     exp.append(p)
     assert np.array_equal(got, np.array(exp).reshape(-1, 3))
+
+
+def test_topk_reductions_and_closed_form():
+    """F3 top-k (north_star "fused top-k/weighted-mean pose update"): topk >= |A| is the paper's
+    mean bit for bit; topk = 1 moves by exactly the best member's delta (smallest E_k, lowest k on
+    ties) -- on the F-track plane the 2.5 cm row (E = 0) wins over the 1.25 cm row."""
+    f = f_track_inputs()
+    vol = oracle.OracleVolume(f["desc"], f["V"], f["W"])
+    pst = np.array([[0, 0, 0, 0, 0, -0.125], [0, 0, 0, 0, 0, -0.25], [0, 0, 0, 0, 0, 0.1]], np.float32)
+    p = dataclasses.replace(f["params"], iters=1)
+    m = vol.track(f["depth"], f["intr"], f["T_init"], pst, p)
+    big = vol.track(f["depth"], f["intr"], f["T_init"], pst, dataclasses.replace(p, update_rule=2, topk=5))
+    assert np.array_equal(m["trace"], big["trace"]) and np.array_equal(m["T"], big["T"])
+    one = vol.track(f["depth"], f["intr"], f["T_init"], pst, dataclasses.replace(p, update_rule=2, topk=1))
+    assert one["trace"][0, 1] == 1
+    assert abs(one["T"][2, 3] - (f["T_init"][2, 3] - 0.025)) < 1e-12
+    # on config T, topk = 8 averages exactly the 8 best members of iteration 1
+    c = config_tiny(seed=1)
+    ct = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    p8 = TrackParams(iters=1, stride=2, update_rule=2, topk=8)
+    r8 = ct.track(c["depth"], c["intr"], c["T_init"], c["pst"], p8)
+    Eb = r8["trace"][0, 0]
+    order = sorted([k for k in range(64) if r8["E"][k] < Eb], key=lambda k: (r8["E"][k], k))[:8]
+    Q, U = np.zeros(4), np.zeros(3)
+    for k in sorted(order):
+        _, q, u = oracle.delta(c["pst"][k], 10.0, 10.0)
+        Q, U = Q + q, U + u
+    Pn = oracle.apply_delta(oracle.quat_to_R(Q / np.linalg.norm(Q)), U / 8, c["T_init"], 0)
+    assert r8["trace"][0, 1] == 8 and np.abs(r8["T"] - Pn).max() < 1e-12
