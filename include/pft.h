@@ -55,7 +55,9 @@ typedef enum { PFT_STORE_F32 = 0, PFT_STORE_F16 = 1 } pft_storage; /* value AND 
 typedef enum { PFT_DELTA_CAMERA_CENTRED = 0, PFT_DELTA_WORLD_LITERAL = 1 } pft_delta_conv;
 
 /* Reading L14: the advantage-set average.  MEAN is the paper's plain mean;
- * WEIGHTED (NEXT F3) weights member k by E_base - E_k > 0.  TOPK returns PFT_ERR_UNSUPPORTED. */
+ * WEIGHTED (NEXT F3) weights member k by E_base - E_k > 0; TOPK (NEXT F3, north_star "top-k")
+ * averages the `topk` (1..32) best members by (E_k, k), plain mean in ascending k; K <= 65536.
+ * With TOPK, trace[1] reports the number of members averaged. */
 typedef enum { PFT_UPDATE_MEAN = 0, PFT_UPDATE_WEIGHTED = 1, PFT_UPDATE_TOPK = 2 } pft_update_rule;
 
 #define PFT_MAX_SCHED 4
@@ -85,7 +87,7 @@ typedef struct {
   double min_inband_frac; /* rho in [0,1]: E = 1 unless n >= rho * N (reading L6; default 0)  */
   pft_delta_conv delta_conv;
   pft_update_rule update_rule;
-  int32_t topk;           /* reserved for PFT_UPDATE_TOPK                                     */
+  int32_t topk;           /* PFT_UPDATE_TOPK: members averaged, 1..32                         */
   /* NEXT F1, the paper's schedule: nsched in [1, PFT_MAX_SCHED] cycles
    * (sched_K, sched_sx, sched_sy): iteration i uses the first min(sched_K, K) template rows and the
    * points of column/row strides (sched_sx, sched_sy); its baseline E(P^(i-1)) is recomputed when

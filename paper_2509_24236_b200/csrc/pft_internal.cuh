@@ -118,6 +118,7 @@ struct TrackLayout {
   size_t ptab_off;     // persistent path: K x 12 folded candidate poses + K flags
   size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
   size_t work_off;     // persistent path: per-iteration work counters
+  size_t topk_off;     // F3 top-k: per-block candidate lists and the merged result
   size_t total;
   int kloc, kfull, nblk_upd;
 };

@@ -195,6 +195,93 @@ __device__ __forceinline__ void member_row(double* row, double E, double Ebase, 
   }
 }
 
+// ---- F3 top-k: (E_k, k) keys.  E >= 0 doubles order like their bit patterns; non-members get ~0.
+constexpr int kTopkMax = 32;
+
+__device__ __forceinline__ bool key_less(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+// Ascending bitonic sort of 256 (key, index) pairs in shared memory (blockDim.x == 256).
+__device__ __forceinline__ void bitonic256(unsigned long long* key, int* idx, int tid) {
+  __syncthreads();
+  for (int k = 2; k <= 256; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int p = tid ^ j;
+      if (p > tid) {
+        const bool up = (tid & k) == 0;
+        const bool gt = key_less(key[p], idx[p], key[tid], idx[tid]);
+        if (up == gt) {
+          const unsigned long long tk = key[tid]; key[tid] = key[p]; key[p] = tk;
+          const int ti = idx[tid]; idx[tid] = idx[p]; idx[p] = ti;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// One 256-particle block's top-k candidates: sorted (key, index) of its members, padded with ~0.
+__device__ __forceinline__ void block_topk(unsigned long long key_mine, int k, int topk, unsigned long long* skey,
+                                           int* sidx, unsigned long long* cand_key, int* cand_idx, int tid) {
+  skey[tid] = key_mine;
+  sidx[tid] = k;
+  bitonic256(skey, sidx, tid);
+  if (tid < topk) { cand_key[tid] = skey[tid]; cand_idx[tid] = sidx[tid]; }
+  __syncthreads();
+}
+
+// Merge of the nblk sorted candidate lists by repeated block-wide minimum of the list heads (one
+// CTA); the selected indices, sorted ascending, then sum their deltas serially in thread 0 (the
+// definition's ascending-k order).  Writes Q(4), U(3), n to out[0..7].
+__device__ __noinline__ void topk_finish(const unsigned long long* cand_key, const int* cand_idx, int nblk, int topk,
+                                         const float* pst, double omega, double v, double* out,
+                                         unsigned long long* skey, int* sidx, int* ssel) {
+  const int tid = threadIdx.x;
+  int head = 0;
+  int nsel = 0;
+  for (int r = 0; r < topk; ++r) {
+    unsigned long long kk = ~0ull;
+    int ii = 0x7fffffff;
+    for (int b = tid; b < nblk; b += 256)
+      if (b == tid && head < topk) {  // each list owned by one thread (nblk <= 256 * ... see below)
+        kk = __ldcg(cand_key + b * kTopkMax + head);
+        ii = __ldcg(cand_idx + b * kTopkMax + head);
+      }
+    skey[tid] = kk;
+    sidx[tid] = ii;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (tid < s && key_less(skey[tid + s], sidx[tid + s], skey[tid], sidx[tid])) {
+        skey[tid] = skey[tid + s];
+        sidx[tid] = sidx[tid + s];
+      }
+      __syncthreads();
+    }
+    const unsigned long long wk = skey[0];
+    const int wi = sidx[0];
+    __syncthreads();
+    if (wk == ~0ull) break;  // no member left
+    if (tid < nblk && kk == wk && ii == wi) ++head;
+    if (tid == 0) ssel[nsel] = wi;
+    ++nsel;
+  }
+  if (tid == 0) {
+    for (int a = 1; a < nsel; ++a)  // insertion sort: ascending particle index
+      for (int b = a; b > 0 && ssel[b - 1] > ssel[b]; --b) { const int t = ssel[b]; ssel[b] = ssel[b - 1]; ssel[b - 1] = t; }
+    double Q[4] = {0.0, 0.0, 0.0, 0.0}, U[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < nsel; ++a) {
+      double q[4], u[3];
+      member_delta(pst + 6 * (size_t)ssel[a], omega, v, q, u);
+      for (int c = 0; c < 4; ++c) Q[c] = Q[c] + 1.0 * q[c];
+      for (int c = 0; c < 3; ++c) U[c] = U[c] + 1.0 * u[c];
+    }
+    for (int c = 0; c < 4; ++c) out[c] = Q[c];
+    for (int c = 0; c < 3; ++c) out[4 + c] = U[c];
+    out[7] = (double)nsel;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ the gather-and-lerp core
 // One 256-bit (fp32) / 128-bit (fp16) load per evaluation: the cell record of the 8 corners.
 __device__ __forceinline__ void ld_rec(const float* p, float (&v)[8]) {
@@ -716,6 +803,10 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
 // (PAPER.md:206), P <- (R(q), u) P.  ceil(K_i/256) CTAs, one particle per thread;
 // each CTA reduces its members in a fixed tree, the last CTA combines the partials in a fixed tree.
 struct UpdArgs {
+  int topk;
+  unsigned long long* ckey;
+  int* cidx;
+  double* tkout;
   TrackState* st;
   const PartRec* full;       // K records (all ranks)
   PartRec* local;            // this rank's records, zeroed for the next iteration
@@ -730,6 +821,8 @@ struct UpdArgs {
 
 __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
   __shared__ double red[kUpdW][256];
+  __shared__ unsigned long long tkey[256];
+  __shared__ int tidx[256], tsel[kTopkMax];
   __shared__ bool sLast;
   TrackState* st = a.st;
   if (st->stopped) return;  // uniform
@@ -740,35 +833,51 @@ __global__ __launch_bounds__(256) void k_update(UpdArgs a) {
   double row[kUpdW];
 #pragma unroll
   for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+  unsigned long long key = ~0ull;
   if (k < a.Ki) {
     const PartRec rec = a.full[k];
     const double E = fitness_of(rec.S, rec.n, a.rho, N);
     a.E_out[k] = E;
     a.n_out[k] = (int)rec.n;
-    member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, st->omega, st->v);
+    if (a.rule == 2) {
+      if (E < Ebase) key = (unsigned long long)__double_as_longlong(E);
+    } else {
+      member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, st->omega, st->v);
+    }
     const int j = k - a.k_begin;
     if (j >= 0 && j < a.kloc) {
       a.local[j].S = 0ull;
       a.local[j].n = 0u;
     }
   }
+  if (a.rule == 2) {
+    block_topk(key, k, a.topk, tkey, tidx, a.ckey + (size_t)blockIdx.x * kTopkMax, a.cidx + (size_t)blockIdx.x * kTopkMax, tid);
+  } else {
 #pragma unroll
-  for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
-  treeW(red, tid);
-  if (tid < kUpdW) a.partials[blockIdx.x * kUpdW + tid] = red[tid][0];
+    for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
+    treeW(red, tid);
+    if (tid < kUpdW) a.partials[blockIdx.x * kUpdW + tid] = red[tid][0];
+  }
   __threadfence();
   __syncthreads();
   if (tid == 0) sLast = atomicAdd(&st->ticket_upd, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!sLast) return;
   __threadfence();
-  // fixed-order combine of the CTA partials
+  if (a.rule == 2) {
+    topk_finish(a.ckey, a.cidx, gridDim.x, a.topk, a.pst, st->omega, st->v, a.tkout, tkey, tidx, tsel);
+    if (tid < 8) red[tid][0] = __ldcg(a.tkout + tid);
+    if (tid == 8) red[8][0] = __ldcg(a.tkout + 7);
+    __syncthreads();
+  } else {
+    // fixed-order combine of the CTA partials
 #pragma unroll
-  for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
-  for (int b = tid; b < (int)gridDim.x; b += 256)
+    for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
+    for (int b = tid; b < (int)gridDim.x; b += 256)
 #pragma unroll
-    for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.partials + b * kUpdW + c);
-  treeW(red, tid);
+      for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.partials + b * kUpdW + c);
+    treeW(red, tid);
+  }
   if (tid == 0) {
     const int nA = (int)red[7][0];
     st->nA = nA;
@@ -840,6 +949,10 @@ struct PArgs {
   unsigned long long* cpart;
   unsigned* work;
   unsigned long long* tdone;   // PFT_PHASE_TIMING: per-CTA P2 finish times (nullptr: off)
+  int topk;
+  unsigned long long* ckey;    // F3 top-k candidates: nblk x kTopkMax (key, index)
+  int* cidx;
+  double* tkout;               // F3 top-k result: Q(4), U(3), n
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -929,8 +1042,10 @@ template <typename T>
 __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   // red (update phases) and sPart (evaluation phase) are never live at the same time
   constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
+  constexpr size_t kTopBytes = 256 * (sizeof(unsigned long long) + sizeof(int));
   constexpr size_t kPartBytes = (kThreads / 32) * kItemParticles * 33 * sizeof(unsigned long long);
-  __shared__ __align__(16) unsigned char sUnion[kRedBytes > kPartBytes ? kRedBytes : kPartBytes];
+  static_assert(kRedBytes + kTopBytes <= kPartBytes, "union layout");
+  __shared__ __align__(16) unsigned char sUnion[kPartBytes];
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12], sPprev[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
@@ -940,6 +1055,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   __shared__ unsigned sNw[kThreads / 32];
   __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
   __shared__ int sWFlag[kThreads / 32][kItemParticles];
+  __shared__ int sTopSel[kTopkMax];
   // per-lane partials of the item's particles: (fix | cnt << 32), rows padded against bank conflicts
   unsigned long long (*sPart)[kItemParticles][33] =
       reinterpret_cast<unsigned long long (*)[kItemParticles][33]>(sUnion);
@@ -1147,36 +1263,57 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     // ---- P3: E_k, advantage set, per-block partials (same tree as k_update)
     const double Ebase = sState[2];
     const int nblk = (Ki + 255) / 256;
+    unsigned long long* tkey = reinterpret_cast<unsigned long long*>(sUnion + kRedBytes);  // top-k scratch
+    int* tidx = reinterpret_cast<int*>(sUnion + kRedBytes + 256 * sizeof(unsigned long long));
     for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
       const int k = b * 256 + tid;
       double row[kUpdW];
 #pragma unroll
       for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+      unsigned long long key = ~0ull;
       if (k < Ki) {
         const unsigned long long S = __ldcg(&a.acc[k].S);
         const unsigned n = __ldcg(&a.acc[k].n);
         const double E = fitness_of(S, n, a.rho, N);
         a.E_out[k] = E;
         a.n_out[k] = (int)n;
-        member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
+        if (a.rule == 2) {
+          if (E < Ebase) key = (unsigned long long)__double_as_longlong(E);
+        } else {
+          member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
+        }
         a.acc[k].S = 0ull;
         a.acc[k].n = 0u;
       }
+      if (a.rule == 2) {
+        block_topk(key, k, a.topk, tkey, tidx, a.ckey + (size_t)b * kTopkMax, a.cidx + (size_t)b * kTopkMax, tid);
+      } else {
 #pragma unroll
-      for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
-      treeW(red, tid);
-      if (tid < kUpdW) a.upart[b * kUpdW + tid] = red[tid][0];
-      __syncthreads();
+        for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
+        treeW(red, tid);
+        if (tid < kUpdW) a.upart[b * kUpdW + tid] = red[tid][0];
+        __syncthreads();
+      }
     }
     grid_barrier(st, gen);
     PFT_TMARK(3);
     // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
+    if (a.rule == 2) {
+      // F3 top-k: CTA 0 merges the blocks' sorted candidates and sums the selected deltas
+      if (blockIdx.x == 0)
+        topk_finish(a.ckey, a.cidx, nblk, a.topk, a.pst, sState[0], sState[1], a.tkout, tkey, tidx, sTopSel);
+      grid_barrier(st, gen);
+      if (tid < 8) red[tid][0] = __ldcg(a.tkout + tid);
+      if (tid == 8) red[8][0] = __ldcg(a.tkout + 7);  // weight sum = number selected
+      __syncthreads();
+    } else {
 #pragma unroll
-    for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
-    for (int b = tid; b < nblk; b += 256)
+      for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
+      for (int b = tid; b < nblk; b += 256)
 #pragma unroll
-      for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.upart + b * kUpdW + c);
-    treeW(red, tid);
+        for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.upart + b * kUpdW + c);
+      treeW(red, tid);
+    }
     if (tid == 0) {
       const int nA = (int)red[7][0];
       sNA = nA;
@@ -1315,6 +1452,8 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
   L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
   L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024 + sizeof(unsigned long long) * 148 * 8, 256);
+  L->topk_off = off;
+  off = align_up(off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)L->nblk_upd + 16 * sizeof(double), 256);
   L->total = off;
   return PFT_OK;
 }
@@ -1432,6 +1571,10 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.work = (unsigned*)(c.ws + c.L.work_off);
   static const bool timing = [] { const char* e = getenv("PFT_PHASE_TIMING"); return e && e[0] == '1'; }();
   pa.tdone = timing ? (unsigned long long*)(c.ws + c.L.work_off + 1024 * sizeof(unsigned)) : nullptr;
+  pa.topk = prm->topk;
+  pa.ckey = (unsigned long long*)(c.ws + c.L.topk_off);
+  pa.cidx = (int*)(c.ws + c.L.topk_off + sizeof(unsigned long long) * kTopkMax * (size_t)c.L.nblk_upd);
+  pa.tkout = (double*)(c.ws + c.L.topk_off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)c.L.nblk_upd);
   void* args[] = {&pa};
   cudaError_t e = cudaSuccess;
   PFT_LAUNCH(PFT_PROF_TRACK, c.st,
@@ -1482,7 +1625,10 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
         if (s != PFT_OK) return s;
       }
     }
-    UpdArgs ua{c.state(), full, local, Ki, k_begin, kloc, pst, prm->delta_conv, prm->update_rule, set,
+    UpdArgs ua{prm->topk, (unsigned long long*)(c.ws + c.L.topk_off),
+               (int*)(c.ws + c.L.topk_off + sizeof(unsigned long long) * kTopkMax * (size_t)c.L.nblk_upd),
+               (double*)(c.ws + c.L.topk_off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)c.L.nblk_upd),
+               c.state(), full, local, Ki, k_begin, kloc, pst, prm->delta_conv, prm->update_rule, set,
                prm->min_inband_frac, E, n_out, (double*)(c.ws + c.L.part_off)};
     PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_update<<<(Ki + 255) / 256, 256, 0, c.st>>>(ua));
     launch_centre<T>(c, 1, set, it, Ki, prm, trace);
@@ -1510,9 +1656,10 @@ static pft_status check_params(const pft_track_params* p) {
   if (!(p->min_inband_frac >= 0.0 && p->min_inband_frac <= 1.0)) return fail(PFT_ERR_INVALID_ARG, "min_inband_frac must be in [0,1]");
   if (p->delta_conv != PFT_DELTA_CAMERA_CENTRED && p->delta_conv != PFT_DELTA_WORLD_LITERAL)
     return fail(PFT_ERR_INVALID_ARG, "bad delta_conv");
-  if (p->update_rule == PFT_UPDATE_TOPK) return fail(PFT_ERR_UNSUPPORTED, "PFT_UPDATE_TOPK is not implemented");
-  if (p->update_rule != PFT_UPDATE_MEAN && p->update_rule != PFT_UPDATE_WEIGHTED)
+  if (p->update_rule != PFT_UPDATE_MEAN && p->update_rule != PFT_UPDATE_WEIGHTED && p->update_rule != PFT_UPDATE_TOPK)
     return fail(PFT_ERR_INVALID_ARG, "bad update_rule");
+  if (p->update_rule == PFT_UPDATE_TOPK && (p->topk < 1 || p->topk > kTopkMax))
+    return fail(PFT_ERR_INVALID_ARG, "topk must be in [1, %d]", kTopkMax);
   if (p->nsched < 0 || p->nsched > PFT_MAX_SCHED) return fail(PFT_ERR_INVALID_ARG, "nsched must be in [0,%d]", PFT_MAX_SCHED);
   if (!(p->min_search_deg >= 0.0) || !(p->min_search_cm >= 0.0)) return fail(PFT_ERR_INVALID_ARG, "min_search must be >= 0");
   if (p->stall_limit < 0) return fail(PFT_ERR_INVALID_ARG, "stall_limit must be >= 0");
@@ -1551,6 +1698,8 @@ pft_status pft_track(pft_volume* vol, const uint16_t* dev_depth, const pft_intri
   if (s != PFT_OK) return s;
   if (ws_bytes < c.L.total) return fail(PFT_ERR_BUFFER_TOO_SMALL, "workspace %zu B < required %zu B", ws_bytes, c.L.total);
   if (((uintptr_t)dev_ws) % 256) return fail(PFT_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (prm->update_rule == PFT_UPDATE_TOPK && nparticles > 256 * 256)
+    return fail(PFT_ERR_UNSUPPORTED, "PFT_UPDATE_TOPK supports at most 65536 particles");
   if (vol->esize == 4)
     return track_run<float>(c, dev_depth, K, dev_T_init, dev_pst, nparticles, prm, dev_T_out, dev_E, dev_inband, dev_trace);
   return track_run<__half>(c, dev_depth, K, dev_T_init, dev_pst, nparticles, prm, dev_T_out, dev_E, dev_inband, dev_trace);

@@ -14,6 +14,9 @@ def main(cfg, seed, out):
     from synth.configs import config_single, config_tiny, with_desc
     import dataclasses
     c = config_tiny(seed=seed) if cfg.startswith("tiny") else config_single(seed=seed)
+    c = dict(c)
+    if cfg == "single_topk":
+        c["params"] = dataclasses.replace(c["params"], update_rule=2, topk=16, iters=5)
     if cfg == "tiny_sched":
         c["params"] = dataclasses.replace(c["params"], iters=7, nsched=3, sched_K=(64, 40, 24, 0),
                                           sched_sx=(1, 2, 4, 0), sched_sy=(1, 2, 2, 0), guard=1, update_rule=1,

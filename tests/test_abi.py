@@ -101,7 +101,9 @@ def test_create_workspace_and_argument_errors(pft):
     assert track(TrackParams(10.0, 10.0, 0.1, 0, 4, 0.0, 0, 0, 0)) == -1       # iters = 0
     assert track(TrackParams(120.0, 10.0, 0.1, 10, 4, 0.0, 0, 0, 0)) == -1     # omega > 100
     assert track(TrackParams(10.0, 10.0, 0.1, 10, 0, 0.0, 0, 0, 0)) == -1      # stride 0
-    assert track(TrackParams(10.0, 10.0, 0.1, 10, 4, 0.0, 0, 2, 0)) == -6      # top-k not implemented
+    assert track(TrackParams(10.0, 10.0, 0.1, 10, 4, 0.0, 0, 2, 0)) == -1      # top-k needs 1 <= topk <= 32
+    assert track(TrackParams(10.0, 10.0, 0.1, 10, 4, 0.0, 0, 2, 33)) == -1
+    assert track(TrackParams(10.0, 10.0, 0.1, 10, 4, 0.0, 0, 3, 0)) == -1      # unknown rule
     assert track(p, ws_bytes=16) == -2                                          # workspace too small
     assert track(p, Kp=0) == -1
     badK = Intrinsics(0.0, 525.0, 319.5, 239.5, 640, 480, 0.001)

@@ -310,7 +310,7 @@ def test_sequence_track_then_integrate(pft):
     vol.close()
 
 
-@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single", "tiny_sched"])
+@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single", "tiny_sched", "single_topk"])
 def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
     """The single-launch persistent tracker (G = 1 default) and the multi-launch path (used for
     G > 1) share their arithmetic helpers and fixed reduction trees: outputs must be bit-identical."""
@@ -331,7 +331,8 @@ def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
 SCHED_TINY = dict(nsched=3, sched_K=(64, 40, 24, 0), sched_sx=(2, 2, 4, 0), sched_sy=(1, 2, 2, 0))
 
 
-@pytest.mark.parametrize("variant", ["schedule", "schedule_guard", "weighted", "weighted_guard_world"])
+@pytest.mark.parametrize("variant", ["schedule", "schedule_guard", "weighted", "weighted_guard_world", "topk",
+                                     "topk_schedule_guard"])
 def test_track_next_rows_tiny(pft, variant):
     """F1 (cycled K / 2-D stride schedule, baseline recomputed on a new point set) and F3 (guard,
     weighted mean) against the oracle: every iteration's trace row and the last E_k / n_k."""
@@ -339,7 +340,8 @@ def test_track_next_rows_tiny(pft, variant):
     c = config_tiny(seed=2)
     base = TrackParams(iters=7, stride=1)
     kw = {"schedule": dict(SCHED_TINY), "schedule_guard": dict(SCHED_TINY, guard=1),
-          "weighted": dict(update_rule=1), "weighted_guard_world": dict(update_rule=1, guard=1, delta_conv=1)}[variant]
+          "weighted": dict(update_rule=1), "weighted_guard_world": dict(update_rule=1, guard=1, delta_conv=1),
+          "topk": dict(update_rule=2, topk=8), "topk_schedule_guard": dict(SCHED_TINY, update_rule=2, topk=5, guard=1)}[variant]
     params = dataclasses.replace(base, **kw)
     vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
     r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], params)
@@ -416,16 +418,19 @@ def test_extract_surface_bit_exact(pft, storage):
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_virtual_shards_bit_identical(pft, G):
+def test_virtual_shards_bit_identical(pft, G):  # noqa: C901
     """SURVEY.md §4 "virtual shards": the multi-GPU code path (rank q evaluates template rows
     [q*ceil(K/G), ...), per-particle records all-gathered, identical update everywhere), emulated on
     one GPU with sequential shards, equals the 1-rank result bit for bit -- on config S and on a
     scheduled/guarded/weighted run with a ragged K."""
     import dataclasses
-    for name in ("single", "tiny_sched"):
+    for name in ("single", "tiny_sched", "single_topk"):
         if name == "single":
             c = config_single(seed=1)
             pst, params = c["pst"], c["params"]
+        elif name == "single_topk":
+            c = config_single(seed=2)
+            pst, params = c["pst"], dataclasses.replace(c["params"], update_rule=2, topk=32, iters=4)
         else:
             c = config_tiny(seed=2)
             pst = make_pst(2, 61)
