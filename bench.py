@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-large", action="store_true", help="skip the config-L (1024^3 fp16) measurement")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                   help="N>1: F2 fused P2P exchange inside the persistent tracker (default) or ncclAllGather")
     return p.parse_args()
 
 
@@ -145,7 +147,10 @@ def run_ours(args):
     for t, d in enumerate(map_depth):
         vol.integrate(torch.from_numpy(d).to(dev), intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
     if world > 1:
-        vol.comm_init()
+        if args.exchange == "p2p":
+            vol.comm_init_p2p(K)
+        else:
+            vol.comm_init()
     pst = torch.from_numpy(seq.pst).to(dev)
     depth_dev = [torch.from_numpy(s["depth"]).to(dev) for s in steps_in]
     tinit_dev = [torch.from_numpy(s["T_init"]).to(dev) for s in steps_in]
@@ -272,6 +277,30 @@ def run_ours(args):
             del pst_s, o2
         vol._ws = {}
 
+    # ---- F2 fused exchange, emulated on this GPU: G rank groups in one persistent launch (same K)
+    fused = {}
+    if world == 1:
+        i0 = idx[0]
+        o3 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(K, dtype=torch.float64, device=dev),
+                  n=torch.empty(K, dtype=torch.int32, device=dev), trace=None)
+        for G in (1, 2, 4, 8):
+            vol.comm_init_virtual(G, fused=True)
+            vol.track(depth_dev[i0], intr, tinit_dev[i0], pst, params, out=o3)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                vol.track(depth_dev[i0], intr, tinit_dev[i0], pst, params, out=o3)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            fused[str(G)] = {"ms_track": statistics.median(ts)}
+        vol.comm_init_virtual(1)
+        vol._ws = {}
+        del o3
+
     # ---- config L: 1024^3 @ 5 mm fp16 volume built by integration, K = 4096 track + integrate per frame
     large = {}
     if world == 1 and not args.no_large:
@@ -320,7 +349,8 @@ def run_ours(args):
         "config": {"workload": "Q: 640x480 frame, 160x120 points, K=2048/GPU, 10 iters, 512^3 @1cm fp32 TSDF, "
                                "track + integrate", "particles": K, "points_per_frame": statistics.mean(n_valid),
                    "iters": ITERS, "volume": "512^3 fp32", "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"particles sharded x{world}, volume replicated"},
+                   "parallelism": f"particles sharded x{world}, volume replicated"
+                   + (f", {args.exchange} exchange" if world > 1 else "")},
         "frame_ms": {"median": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
                      "max": max(per_step)},
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
@@ -334,6 +364,7 @@ def run_ours(args):
                      "evals_per_s_kernel": evals_per_launch / avg_launch_s},
         "clocks": clk.summary(),
         "particle_sweep": sweep,
+        "fused_exchange_emulation": fused,
         "large_volume": large,
         "pose_err_vs_gt": {"rot_deg_median": statistics.median(rot_err), "rot_deg_p90": float(np.percentile(rot_err, 90)),
                            "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PFT_ABI_VERSION 2
+#define PFT_ABI_VERSION 3
 
 typedef enum {
   PFT_OK = 0,
@@ -233,6 +233,32 @@ pft_status pft_comm_get_unique_id(uint8_t id_out[128]);
  * calls pft_integrate with the same inputs.  The current CUDA device must be this rank's. */
 pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks, int32_t rank);
 
+/* F2 fused exchange (Sec. III-C "Randomized optimization": every
+ * particle's E_k is needed by every rank for the advantage-set update).  With peer buffers
+ * attached, pft_track runs the whole RO loop as one persistent launch per GPU: each rank
+ * evaluates its shard (rows [r*ceil(K/G), ...)), then its CTAs store their finished per-particle
+ * records (16 B each) straight into every rank's exchange buffer over NVLink (P2P stores), the
+ * rank signals each peer with one system-scope atomic, and waits for all G shards before the
+ * update -- no NCCL launch and no host round trip per iteration.  Counters are monotone across
+ * calls (each rank stores the number of completed rounds in its own buffer), so calls need no
+ * reset handshake; all ranks must call pft_track with the same arguments the same number of
+ * times.  A rank that waits more than 5 s for a peer traps (launch error instead of a hang).
+ *
+ * pft_comm_p2p_init: allocates (cudaMalloc, zero-filled) this rank's exchange buffer sized for
+ *   up to max_particles particles and nranks <= PFT_MAX_FUSED_RANKS ranks, and writes its
+ *   CUDA IPC handle (PFT_IPC_HANDLE_BYTES) to handle_out.  The library owns the buffer (freed
+ *   by pft_volume_destroy).  Call on the rank's own device.
+ * pft_comm_p2p_attach: `handles` = the nranks handles in rank order (gathered by the caller,
+ *   e.g. torch.distributed.all_gather); opens the peers' buffers with peer access enabled.  The
+ *   caller must barrier all ranks after attach and before the first pft_track.
+ * Errors: PFT_ERR_STATE if another communicator is attached; PFT_ERR_CUDA if IPC fails (the
+ * GPUs must be peers on one node). */
+#define PFT_MAX_FUSED_RANKS 8
+#define PFT_IPC_HANDLE_BYTES 64
+pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int32_t max_particles,
+                             uint8_t handle_out[PFT_IPC_HANDLE_BYTES]);
+pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles);
+
 /* ---------------------------------------------------------------- instrumentation */
 
 /* Kernel classes of the per-launch profile. */
@@ -245,7 +271,7 @@ pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks,
 #define PFT_PROF_COMM 6        /* ncclAllGather (a6)                                          */
 #define PFT_PROF_OTHER 7       /* volume reset / upload / download / checksum                 */
 #define PFT_PROF_RECORDS 8     /* tracker cell-record / in-band-mask maintenance (a10)        */
-#define PFT_PROF_TRACK 9       /* k_track_persistent: the whole RO loop in one launch (G = 1) */
+#define PFT_PROF_TRACK 9       /* k_track_persistent: the whole RO loop in one launch         */
 #define PFT_PROF_CLASSES 10
 
 /* Cumulative number of CUDA kernels (and NCCL collectives) this library has launched. */
@@ -263,6 +289,13 @@ pft_status pft_profile_stop(double* ms_out, int64_t* launches_out);
  * all-gather replaced by device copies; results must equal the 1-rank run bit for bit.  Not for
  * production (the shards run sequentially). */
 pft_status pft_comm_init_virtual(pft_volume* vol, int32_t nranks);
+
+/* Test/debug: emulate the F2 fused exchange on this one GPU: pft_track runs ONE persistent
+ * launch holding nranks (<= PFT_MAX_FUSED_RANKS) groups of CTAs, each group a rank with its own
+ * workspace region (pft_track_workspace_bytes grows nranks-fold) and exchange buffer, pushing
+ * its shard into every group's buffer and waiting on the same counters the multi-GPU path uses.
+ * Results (T, E, n, trace) must equal the 1-rank run bit for bit; group 0 writes the outputs. */
+pft_status pft_comm_init_virtual_fused(pft_volume* vol, int32_t nranks);
 
 /* Thread-local message describing the last non-OK status of this thread. */
 const char* pft_last_error(void);

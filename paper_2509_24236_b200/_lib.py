@@ -10,6 +10,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PFT_LIB") or os.path.join(HERE, "libpft.so")
 TRACE_DOUBLES = 24
+IPC_HANDLE_BYTES = 64          # include/pft.h PFT_IPC_HANDLE_BYTES
+MAX_FUSED_RANKS = 8            # include/pft.h PFT_MAX_FUSED_RANKS
 INTEGRATE_FULL_SWEEP = 1
 
 STATUS = {0: "PFT_OK", -1: "PFT_ERR_INVALID_ARG", -2: "PFT_ERR_BUFFER_TOO_SMALL", -3: "PFT_ERR_EMPTY_CLOUD",
@@ -19,7 +21,8 @@ STATUS = {0: "PFT_OK", -1: "PFT_ERR_INVALID_ARG", -2: "PFT_ERR_BUFFER_TOO_SMALL"
 EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_volume_upload", "pft_volume_download",
            "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_extract_surface",
            "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
-           "pft_comm_init", "pft_comm_init_virtual", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
+           "pft_comm_init", "pft_comm_init_virtual", "pft_comm_init_virtual_fused", "pft_comm_p2p_init",
+           "pft_comm_p2p_attach", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
 PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records", "track"]
 
@@ -80,6 +83,9 @@ def lib():
         "pft_comm_get_unique_id": [P],
         "pft_comm_init": [P, P, I32, I32],
         "pft_comm_init_virtual": [P, I32],
+        "pft_comm_init_virtual_fused": [P, I32],
+        "pft_comm_p2p_init": [P, I32, I32, I32, P],
+        "pft_comm_p2p_attach": [P, P],
         "pft_profile_start": [],
         "pft_profile_stop": [P, P],
     }

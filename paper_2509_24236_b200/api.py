@@ -7,7 +7,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import (INTEGRATE_FULL_SWEEP, TRACE_DOUBLES, Intrinsics, TrackParams, VolumeDesc, check, lib)
+from ._lib import (INTEGRATE_FULL_SWEEP, IPC_HANDLE_BYTES, TRACE_DOUBLES, Intrinsics, TrackParams, VolumeDesc, check, lib)
 
 STORE = {"f32": 0, "f16": 1, 0: 0, 1: 1}
 
@@ -188,10 +188,27 @@ class Volume:
         self.nranks, self.rank = world, rank
         self._ws = {}
 
-    def comm_init_virtual(self, nranks):
-        """Test/debug: run the multi-GPU path with nranks sequential shards on this GPU."""
-        check(lib().pft_comm_init_virtual(self.handle, int(nranks)))
+    def comm_init_virtual(self, nranks, fused=False):
+        """Test/debug: run the multi-GPU path with nranks shards on this GPU -- sequential shard
+        launches + device copies (fused=False), or the F2 fused exchange with nranks rank groups
+        of CTAs in one persistent launch (fused=True)."""
+        fn = lib().pft_comm_init_virtual_fused if fused else lib().pft_comm_init_virtual
+        check(fn(self.handle, int(nranks)))
         self.nranks, self.rank = int(nranks), 0
+        self._ws = {}
+
+    def comm_init_p2p(self, max_particles, group=None):
+        """F2 fused exchange over NVLink peer memory: allocate this rank's exchange buffer, gather
+        every rank's CUDA IPC handle over torch.distributed `group`, open the peers', barrier."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        h = (C.c_uint8 * IPC_HANDLE_BYTES)()
+        check(lib().pft_comm_p2p_init(self.handle, world, rank, int(max_particles), h))
+        handles = gather_handles(bytes(h), group)
+        raw = (C.c_uint8 * (IPC_HANDLE_BYTES * world))(*handles)
+        check(lib().pft_comm_p2p_attach(self.handle, raw))
+        dist.barrier(group=group)
+        self.nranks, self.rank = world, rank
         self._ws = {}
 
     def close(self):
@@ -204,6 +221,20 @@ class Volume:
             self.close()
         except Exception:
             pass
+
+
+def gather_handles(mine, group=None):
+    """All ranks' IPC handles (IPC_HANDLE_BYTES each) concatenated in rank order, as a byte string.
+    Host-side plumbing only (tests/test_multirank.py exercises it over gloo)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    assert len(mine) == IPC_HANDLE_BYTES
+    t = torch.tensor(list(mine), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(torch.device("cuda", torch.cuda.current_device()))
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return b"".join(bytes(o.cpu().tolist()) for o in out)
 
 
 def shard_range(K, nranks, rank):

@@ -181,6 +181,10 @@ pft_status pft_volume_destroy(pft_volume* vol) {
     Nccl* n = nccl();
     if (n) n->commDestroy((ncclComm_t)vol->nccl_comm);
   }
+  if (vol->p2p)
+    for (int q = 0; q < vol->nranks; ++q)
+      if (q != vol->rank && vol->xbuf[q]) cudaIpcCloseMemHandle(vol->xbuf[q]);
+  if (vol->xown) cudaFree(vol->xown);
   delete vol;
   return PFT_OK;
 }
@@ -200,9 +204,80 @@ pft_status pft_comm_init_virtual(pft_volume* vol, int32_t nranks) {
   if (!vol) return fail(PFT_ERR_INVALID_ARG, "vol is NULL");
   if (nranks < 1) return fail(PFT_ERR_INVALID_ARG, "nranks must be >= 1");
   if (vol->nccl_comm) return fail(PFT_ERR_STATE, "a real communicator is attached");
+  if (vol->p2p) return fail(PFT_ERR_STATE, "peer exchange buffers are attached");
   vol->nranks = nranks;
   vol->rank = 0;
   vol->virtual_ranks = nranks > 1 ? nranks : 0;
+  vol->virtual_fused = 0;
+  return PFT_OK;
+}
+
+pft_status pft_comm_init_virtual_fused(pft_volume* vol, int32_t nranks) {
+  if (!vol) return fail(PFT_ERR_INVALID_ARG, "vol is NULL");
+  if (nranks < 1 || nranks > PFT_MAX_FUSED_RANKS)
+    return fail(PFT_ERR_INVALID_ARG, "nranks must be in [1,%d]", PFT_MAX_FUSED_RANKS);
+  if (vol->nccl_comm) return fail(PFT_ERR_STATE, "a real communicator is attached");
+  if (vol->p2p) return fail(PFT_ERR_STATE, "peer exchange buffers are attached");
+  vol->nranks = nranks;
+  vol->rank = 0;
+  vol->virtual_ranks = nranks > 1 ? nranks : 0;
+  vol->virtual_fused = nranks > 1 ? 1 : 0;
+  vol->xws_last = nullptr;
+  vol->xws_total = 0;
+  return PFT_OK;
+}
+
+pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int32_t max_particles,
+                             uint8_t handle_out[PFT_IPC_HANDLE_BYTES]) {
+  if (!vol || !handle_out) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  if (nranks < 2 || nranks > PFT_MAX_FUSED_RANKS)
+    return fail(PFT_ERR_INVALID_ARG, "nranks must be in [2,%d]", PFT_MAX_FUSED_RANKS);
+  if (rank < 0 || rank >= nranks) return fail(PFT_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+  if (max_particles < 1) return fail(PFT_ERR_INVALID_ARG, "max_particles must be >= 1");
+  if (vol->p2p || vol->xown) return fail(PFT_ERR_STATE, "peer exchange already initialised");
+  if (vol->nccl_comm || vol->virtual_ranks) return fail(PFT_ERR_STATE, "another communicator is attached");
+  const size_t kloc = ((size_t)max_particles + nranks - 1) / nranks;
+  const size_t rec = (2 * sizeof(pft::PartRec) * kloc * (size_t)nranks + 255) / 256 * 256;
+  const size_t bytes = rec + (pft::kMaxFusedRanks + 1) * sizeof(unsigned long long);
+  char* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "exchange buffer (%zu B): %s", bytes, cudaGetErrorString(e));
+  e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(PFT_ERR_CUDA, "exchange buffer IPC handle: %s", cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == PFT_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  vol->xown = p;
+  vol->xbytes = bytes;
+  vol->xcnt_off = rec;
+  vol->xmax_particles = max_particles;
+  vol->nranks = nranks;
+  vol->rank = rank;
+  return PFT_OK;
+}
+
+pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles) {
+  if (!vol || !handles) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  if (!vol->xown) return fail(PFT_ERR_STATE, "pft_comm_p2p_init was not called");
+  if (vol->p2p) return fail(PFT_ERR_STATE, "peers already attached");
+  for (int q = 0; q < vol->nranks; ++q) {
+    if (q == vol->rank) { vol->xbuf[q] = vol->xown; continue; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + (size_t)q * PFT_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int r = 0; r < q; ++r)
+        if (r != vol->rank && vol->xbuf[r]) { cudaIpcCloseMemHandle(vol->xbuf[r]); vol->xbuf[r] = nullptr; }
+      return fail(PFT_ERR_CUDA, "opening rank %d's exchange buffer: %s", q, cudaGetErrorString(e));
+    }
+    vol->xbuf[q] = (char*)p;
+  }
+  vol->p2p = 1;
   return PFT_OK;
 }
 

@@ -53,6 +53,10 @@ struct VolLayout {
 
 }  // namespace pft
 
+namespace pft {
+constexpr int kMaxFusedRanks = PFT_MAX_FUSED_RANKS;  // F2 fused exchange: ranks per job
+}
+
 struct pft_volume {
   pft_volume_desc desc;
   pft::Geom g;
@@ -64,6 +68,17 @@ struct pft_volume {
   void* nccl_comm;
   int nranks, rank;
   int virtual_ranks;  // > 1: pft_comm_init_virtual (sequential shards, no NCCL)
+  int virtual_fused;  // pft_comm_init_virtual_fused: G rank groups in one persistent launch
+  // F2 peer exchange (pft_comm_p2p_init / _attach): xbuf[q] = rank q's exchange buffer mapped
+  // into this process (xbuf[rank] = xown); records at 0, counters at xcnt_off
+  int p2p;
+  char* xbuf[PFT_MAX_FUSED_RANKS];
+  char* xown;
+  size_t xbytes, xcnt_off;
+  int32_t xmax_particles;
+  // one-GPU emulation: the exchange counters are zeroed when the workspace changes
+  const char* xws_last;
+  size_t xws_total;
 };
 
 namespace pft {
@@ -119,7 +134,10 @@ struct TrackLayout {
   size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
   size_t work_off;     // persistent path: per-iteration work counters
   size_t topk_off;     // F3 top-k: per-block candidate lists and the merged result
-  size_t total;
+  size_t total;         // bytes of the whole workspace (G regions in the fused emulation)
+  size_t region;        // bytes of one rank's region
+  size_t xch_off;       // fused emulation: the rank's exchange buffer inside its region
+  size_t xcnt_rel;      //   its counters: kMaxFusedRanks words + the completed-round word
   int kloc, kfull, nblk_upd;
 };
 

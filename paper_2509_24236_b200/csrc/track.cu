@@ -937,23 +937,30 @@ struct PArgs {
   double beta, rho, omega0, v0;
   StopRule sr;
   const double* T_init;
-  TrackState* st;
-  PartRec* acc;
   double* E_out;
   int* n_out;
   double* trace;
   double* T_out;
-  double* ptab;
-  int* pflag;
-  double* upart;
-  unsigned long long* cpart;
-  unsigned* work;
   unsigned long long* tdone;   // PFT_PHASE_TIMING: per-CTA P2 finish times (nullptr: off)
   int topk;
-  unsigned long long* ckey;    // F3 top-k candidates: nblk x kTopkMax (key, index)
-  int* cidx;
-  double* tkout;               // F3 top-k result: Q(4), U(3), n
+  // workspace: rank r's region starts at ws + r * rank_stride in one-GPU emulation (emul = 1),
+  // at ws on its own GPU otherwise; the o_* are byte offsets inside a region
+  char* ws;
+  size_t rank_stride;
+  size_t o_state, o_acc, o_ptab, o_pflag, o_upart, o_cpart, o_work;
+  size_t o_ckey, o_cidx, o_tkout;  // F3 top-k candidates nblk x kTopkMax (key, index); result Q(4), U(3), n
+  // F2 fused exchange (G > 1): xbuf[r] = rank r's exchange buffer (Kpad PartRec records, then
+  // kXchgWords counter words), a peer pointer on a real multi-GPU node
+  int G, rank, emul;
+  char* xbuf[kMaxFusedRanks];
+  size_t o_xcnt;
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -964,12 +971,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // Sense-reversing grid barrier over co-resident CTAs; the gpu-scope fences also invalidate L1
 // (CCTL.IVALL) so data written by other CTAs before the barrier is read fresh after it.
 // Watchdog: a CTA that waits more than 5 s traps (a launch error instead of a hung GPU).
-__device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
+__device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen, int nb) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned arrived = atomicAdd(&st->bar_count, 1u);
-    if (arrived == gridDim.x - 1) {
+    if (arrived == (unsigned)nb - 1u) {
       st->bar_count = 0u;
       __threadfence();
       atomicExch(&st->bar_gen, gen + 1u);
@@ -992,9 +999,9 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned& gen) {
 template <typename T>
 __device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsigned long long* __restrict__ mask,
                                              const Geom& g, const Points& pts, const double* m, int flag,
-                                             unsigned long long& sum, unsigned& cnt) {
-  const int per = (pts.npad + gridDim.x - 1) / gridDim.x;
-  const int b0 = blockIdx.x * per, b1 = min(pts.npad, b0 + per);
+                                             int nb, int lb, unsigned long long& sum, unsigned& cnt) {
+  const int per = (pts.npad + nb - 1) / nb;
+  const int b0 = lb * per, b1 = min(pts.npad, b0 + per);
   for (int base = b0; base < b1; base += kThreads) {
     const int i = base + threadIdx.x;
     double px[1] = {0.0}, py[1] = {0.0}, pz[1] = {0.0};
@@ -1063,31 +1070,61 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   // make the compiler spill the whole parameter block to local memory
   __shared__ PSet sSets[PFT_MAX_SCHED];
   __shared__ int sSchedK[PFT_MAX_SCHED], sSchedSet[PFT_MAX_SCHED];
-  TrackState* st = a.st;
+  // F2 rank groups: G ranks; in one-GPU emulation the grid holds all G groups of nb CTAs each and
+  // every group owns a workspace region (a real multi-GPU run has one group per GPU)
+  const int G = a.G;
+  const int nb = a.emul ? (int)gridDim.x / G : (int)gridDim.x;   // CTAs of this rank
+  const int grp = a.emul ? (int)blockIdx.x / nb : a.rank;       // this rank
+  const int lb = a.emul ? (int)blockIdx.x - grp * nb : (int)blockIdx.x;
+  char* const wsb = a.ws + (a.emul ? (size_t)grp * a.rank_stride : 0);
+  const size_t wsoff = (size_t)(wsb - a.ws);
+  TrackState* st = (TrackState*)(wsb + a.o_state);
+  PartRec* const acc = (PartRec*)(wsb + a.o_acc);                // this rank's shard accumulators
+  double* const ptab = (double*)(wsb + a.o_ptab);
+  int* const pflag = (int*)(wsb + a.o_pflag);
+  double* const upart = (double*)(wsb + a.o_upart);
+  unsigned long long* const cpart = (unsigned long long*)(wsb + a.o_cpart);
+  unsigned* const work = (unsigned*)(wsb + a.o_work);
+  unsigned long long* const ckey = (unsigned long long*)(wsb + a.o_ckey);
+  int* const cidx = (int*)(wsb + a.o_cidx);
+  double* const tkout = (double*)(wsb + a.o_tkout);
+  const bool out_rank = !a.emul || grp == 0;                     // writes the caller's outputs
+  const int kloc = (a.K + G - 1) / G, kb = grp * kloc;            // shard: rows [kb, kb + kloc)
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned gen = 0u;
   // PFT_PHASE_TIMING accumulators (CTA 0, thread 0): B, P1, P2, P3, P4, P5, P2 tail, P0
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tmark = 0;
   const bool timing = a.tdone != nullptr;
   if (timing && tid == 0) tmark = global_ns();
+  __shared__ unsigned long long sXround;
+  __shared__ char* sXbuf[kMaxFusedRanks];  // (dynamic indexing of the parameter copy would spill it)
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < kMaxFusedRanks; ++q) sXbuf[q] = a.xbuf[q];
+  }
+  __syncthreads();
   if (tid == 0) {
     gen = *(volatile unsigned*)&st->bar_gen;
+    sXround = G > 1 ? *(volatile unsigned long long*)(sXbuf[grp] + a.o_xcnt + kMaxFusedRanks * sizeof(unsigned long long)) : 0ull;
 #pragma unroll
     for (int q = 0; q < PFT_MAX_SCHED; ++q) {
-      sSets[q] = a.sc.sets[q];
+      PSet p = a.sc.sets[q];
+      if (p.x) { p.x = (double*)((char*)p.x + wsoff); p.y = (double*)((char*)p.y + wsoff); p.z = (double*)((char*)p.z + wsoff); }
+      sSets[q] = p;
       sSchedK[q] = a.sc.K[q];
       sSchedSet[q] = a.sc.set[q];
     }
   }
   __syncthreads();
   const int nsched = a.sc.n, nsets = a.sc.nsets;
+  const unsigned long long xround0 = sXround;
   // ---- P0: points of every set (a1/a2), accumulators, pmax
   {
-    const int stride = gridDim.x * kThreads;
+    const int stride = nb * kThreads;
     double pm = 0.0;
     for (int sidx = 0; sidx < nsets; ++sidx) {
       const PSet ps = sSets[sidx];
-      for (int i0 = blockIdx.x * kThreads; i0 < ps.npad; i0 += stride) {
+      for (int i0 = lb * kThreads; i0 < ps.npad; i0 += stride) {
         const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
         double X = 0.0, Y = 0.0, Z = 0.0;
         bool valid = false;
@@ -1102,14 +1139,14 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     }
     for (int sft = 16; sft > 0; sft >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, sft));
     if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
-    for (int k = blockIdx.x * kThreads + tid; k < a.K; k += stride) { a.acc[k].S = 0ull; a.acc[k].n = 0u; }
+    for (int k = lb * kThreads + tid; k < kloc; k += stride) { acc[k].S = 0ull; acc[k].n = 0u; }
   }
   if (tid == 0) {
     for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
     sState[0] = a.omega0; sState[1] = a.v0; sState[2] = 1.0;
     sStalls = 0; sStop = 0; sSet = -1; sKlast = 0; sNc = 0u; sNA = 0;
   }
-  grid_barrier(st, gen);
+  grid_barrier(st, gen, nb);
 #define PFT_TMARK(slot)                                        \
   if (timing && tid == 0) {                                    \
     const unsigned long long now_ = global_ns();               \
@@ -1131,15 +1168,15 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       __syncthreads();
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, sum, cnt);
+      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
       // half 0 of the centre partials: P5 of the previous iteration may still be reading half 1
-      if (tid == 0) { a.cpart[2 * blockIdx.x] = S; a.cpart[2 * blockIdx.x + 1] = n; }
-      grid_barrier(st, gen);
+      if (tid == 0) { cpart[2 * lb] = S; cpart[2 * lb + 1] = n; }
+      grid_barrier(st, gen, nb);
       unsigned long long S2, n2;
-      sum_partials(a.cpart, gridDim.x, sS, sNw, S2, n2);
+      sum_partials(cpart, nb, sS, sNw, S2, n2);
       if (tid == 0) {
         sState[2] = fitness_c(S2, (unsigned)n2, a.rho, N);
         sNc = (unsigned)n2;
@@ -1149,15 +1186,17 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     }
     PFT_TMARK(0);
     // ---- P1: candidate-pose table (K_i rows)
-    for (int k = blockIdx.x * kThreads + tid; k < Ki; k += gridDim.x * kThreads) {
+    for (int k = kb + lb * kThreads + tid; k < min(Ki, kb + kloc); k += nb * kThreads) {
       double m[12];
-      a.pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
-      double2* row = (double2*)(a.ptab + 12 * (size_t)k);
+      pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
+      double2* row = (double2*)(ptab + 12 * (size_t)k);
 #pragma unroll
       for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
     }
-    grid_barrier(st, gen);
+    grid_barrier(st, gen, nb);
     PFT_TMARK(1);
+    // F2: this rank's shard of the K_i particles, local rows [0, Ks) = global rows [kb, kb + Ks)
+    const int Ks = max(0, min(Ki, kb + kloc) - kb);
     // ---- P2: particle x point evaluation, warp-granular items (group-major: item = group * nchunks
     // + chunk).  sched 0: one global dynamic queue; sched 1: CTA c owns the contiguous range
     // [c*n/G, (c+1)*n/G) (its warps share one image region -> L1 reuse), handed out by a CTA counter.
@@ -1165,21 +1204,21 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       // Items: the first ~80% of the particle chunks as 16-particle items, the rest as 4-particle
       // items handed out last, so the queue drains on small items (short cross-CTA tail).
       const int ngroups = (pts.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
-      const int nch16 = (Ki + kItemParticles - 1) / kItemParticles;
+      const int nch16 = (Ks + kItemParticles - 1) / kItemParticles;
       // (only when there are few items per warp: with many, the tail is already negligible)
-      const bool few = (long long)ngroups * nch16 < 64LL * gridDim.x * (kThreads / 32);
+      const bool few = (long long)ngroups * nch16 < 64LL * nb * (kThreads / 32);
       const int cb = (a.sched == 1 || !few) ? nch16 : nch16 - (nch16 * a.tail_pct + 99) / 100;  // big chunks
       const int ksmall = cb * kItemParticles;                           // first particle of the small part
-      const int nch4 = (Ki - ksmall + 3) / 4;
+      const int nch4 = (Ks - ksmall + 3) / 4;
       const int nbig = ngroups * cb;
       const int nitems = nbig + ngroups * nch4;
-      const int r0 = (int)((long long)nitems * blockIdx.x / gridDim.x);
-      const int r1 = (int)((long long)nitems * (blockIdx.x + 1) / gridDim.x);
+      const int r0 = (int)((long long)nitems * lb / nb);
+      const int r1 = (int)((long long)nitems * (lb + 1) / nb);
       if (tid == 0) sItem = 0;
       __syncthreads();
       for (;;) {
         int item = 0;
-        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(a.work + it, 1u);
+        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(work + it, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (a.sched == 1 ? r1 : nitems)) break;
         int group, k0, k1;
@@ -1187,13 +1226,13 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
           group = item / cb;
           const int chunk = item - group * cb;
           k0 = chunk * kItemParticles;
-          k1 = min(Ki, k0 + kItemParticles);
+          k1 = min(Ks, k0 + kItemParticles);
         } else {
           const int it2 = item - nbig;
           group = it2 / nch4;
           const int chunk = it2 - group * nch4;
           k0 = ksmall + chunk * 4;
-          k1 = min(Ki, k0 + 4);
+          k1 = min(Ks, k0 + 4);
         }
         double px[kItemTiles], py[kItemTiles], pz[kItemTiles];
 #pragma unroll
@@ -1206,8 +1245,8 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         double2* wp = sWPose[tid >> 5];
         int* wf = sWFlag[tid >> 5];
         __syncwarp();
-        for (int q = lane; q < (k1 - k0) * 6; q += 32) wp[q] = __ldcg((const double2*)(a.ptab + 12 * (size_t)k0) + q);
-        if (lane < k1 - k0) wf[lane] = __ldcg(a.pflag + k0 + lane);
+        for (int q = lane; q < (k1 - k0) * 6; q += 32) wp[q] = __ldcg((const double2*)(ptab + 12 * (size_t)(kb + k0)) + q);
+        if (lane < k1 - k0) wf[lane] = __ldcg(pflag + kb + k0 + lane);
         __syncwarp();
         unsigned long long (*part)[33] = sPart[tid >> 5];
         for (int k = k0; k < k1; ++k) {
@@ -1238,8 +1277,8 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
             n += (unsigned)(w >> 32);
           }
           if (n) {
-            atomicAdd(&a.acc[k0 + lane].S, S);
-            atomicAdd(&a.acc[k0 + lane].n, n);
+            atomicAdd(&acc[k0 + lane].S, S);
+            atomicAdd(&acc[k0 + lane].n, n);
           }
         }
         __syncwarp();
@@ -1247,12 +1286,12 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     }
     if (timing) {
       __syncthreads();
-      if (tid == 0) a.tdone[blockIdx.x] = global_ns();
+      if (tid == 0) a.tdone[lb] = global_ns();
     }
-    grid_barrier(st, gen);
-    if (timing && tid == 0 && blockIdx.x == 0) {
+    grid_barrier(st, gen, nb);
+    if (timing && tid == 0 && lb == 0) {
       unsigned long long lo = ~0ull, hi = 0ull;
-      for (int b = 0; b < (int)gridDim.x; ++b) {
+      for (int b = 0; b < (int)nb; ++b) {
         const unsigned long long v = __ldcg(a.tdone + b);
         lo = v < lo ? v : lo;
         hi = v > hi ? v : hi;
@@ -1260,58 +1299,99 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       tph[6] += hi - lo;
     }
     PFT_TMARK(2);
+    // ---- X (F2, G > 1): every CTA pushes its slice of this rank's shard records into every rank's
+    // exchange buffer (P2P stores) in the half of the round's parity -- a peer may still be reading
+    // the other half in its P3 of the previous round, possibly of the previous call, but not this
+    // half's previous round (it signalled round R-1 after finishing P3 of round R-2) -- then the
+    // rank signals each peer once and every CTA waits until all G shards of the round arrived.
+    const PartRec* recs = acc;
+    if (G > 1) {
+      const size_t half = (size_t)((xround0 + (unsigned long long)it) & 1ull) * (size_t)G * kloc;  // global round parity
+      for (int j = lb * kThreads + tid; j < Ks; j += nb * kThreads) {
+        const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2*>(acc + j));  // (S, n | pad)
+        for (int q = 0; q < G; ++q) __stcg(reinterpret_cast<ulonglong2*>((PartRec*)sXbuf[q] + half + kb + j), r);
+        acc[j].S = 0ull;
+        acc[j].n = 0u;
+      }
+      __threadfence_system();
+      grid_barrier(st, gen, nb);
+      if (lb == 0 && tid < G) {
+        __threadfence_system();
+        atomicAdd_system((unsigned long long*)(sXbuf[tid] + a.o_xcnt) + grp, 1ull);
+      }
+      if (tid == 0) {
+        const unsigned long long* cnt = (const unsigned long long*)(sXbuf[grp] + a.o_xcnt);
+        const unsigned long long target = xround0 + (unsigned long long)it + 1ull;
+        const unsigned long long t0 = global_ns();
+        for (int q = 0; q < G; ++q)
+          while (ld_acquire_sys(cnt + q) < target) {
+            __nanosleep(32);
+            if (global_ns() - t0 > 5000000000ull) {
+              printf("pft: exchange timeout (rank %d CTA %d source %d round %llu)\n", grp, lb, q, target);
+              __trap();
+            }
+          }
+        __threadfence_system();
+      }
+      __syncthreads();
+      recs = (const PartRec*)sXbuf[grp] + half;
+    }
     // ---- P3: E_k, advantage set, per-block partials (same tree as k_update)
     const double Ebase = sState[2];
     const int nblk = (Ki + 255) / 256;
     unsigned long long* tkey = reinterpret_cast<unsigned long long*>(sUnion + kRedBytes);  // top-k scratch
     int* tidx = reinterpret_cast<int*>(sUnion + kRedBytes + 256 * sizeof(unsigned long long));
-    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    for (int b = lb; b < nblk; b += nb) {
       const int k = b * 256 + tid;
       double row[kUpdW];
 #pragma unroll
       for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
       unsigned long long key = ~0ull;
       if (k < Ki) {
-        const unsigned long long S = __ldcg(&a.acc[k].S);
-        const unsigned n = __ldcg(&a.acc[k].n);
+        const unsigned long long S = __ldcg(&recs[k].S);
+        const unsigned n = __ldcg(&recs[k].n);
         const double E = fitness_of(S, n, a.rho, N);
-        a.E_out[k] = E;
-        a.n_out[k] = (int)n;
+        if (out_rank) {
+          a.E_out[k] = E;
+          a.n_out[k] = (int)n;
+        }
         if (a.rule == 2) {
           if (E < Ebase) key = (unsigned long long)__double_as_longlong(E);
         } else {
           member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
         }
-        a.acc[k].S = 0ull;
-        a.acc[k].n = 0u;
+        if (G == 1) {
+          acc[k].S = 0ull;
+          acc[k].n = 0u;
+        }
       }
       if (a.rule == 2) {
-        block_topk(key, k, a.topk, tkey, tidx, a.ckey + (size_t)b * kTopkMax, a.cidx + (size_t)b * kTopkMax, tid);
+        block_topk(key, k, a.topk, tkey, tidx, ckey + (size_t)b * kTopkMax, cidx + (size_t)b * kTopkMax, tid);
       } else {
 #pragma unroll
         for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
         treeW(red, tid);
-        if (tid < kUpdW) a.upart[b * kUpdW + tid] = red[tid][0];
+        if (tid < kUpdW) upart[b * kUpdW + tid] = red[tid][0];
         __syncthreads();
       }
     }
-    grid_barrier(st, gen);
+    grid_barrier(st, gen, nb);
     PFT_TMARK(3);
     // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
     if (a.rule == 2) {
       // F3 top-k: CTA 0 merges the blocks' sorted candidates and sums the selected deltas
-      if (blockIdx.x == 0)
-        topk_finish(a.ckey, a.cidx, nblk, a.topk, a.pst, sState[0], sState[1], a.tkout, tkey, tidx, sTopSel);
-      grid_barrier(st, gen);
-      if (tid < 8) red[tid][0] = __ldcg(a.tkout + tid);
-      if (tid == 8) red[8][0] = __ldcg(a.tkout + 7);  // weight sum = number selected
+      if (lb == 0)
+        topk_finish(ckey, cidx, nblk, a.topk, a.pst, sState[0], sState[1], tkout, tkey, tidx, sTopSel);
+      grid_barrier(st, gen, nb);
+      if (tid < 8) red[tid][0] = __ldcg(tkout + tid);
+      if (tid == 8) red[8][0] = __ldcg(tkout + 7);  // weight sum = number selected
       __syncthreads();
     } else {
 #pragma unroll
       for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
       for (int b = tid; b < nblk; b += 256)
 #pragma unroll
-        for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(a.upart + b * kUpdW + c);
+        for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(upart + b * kUpdW + c);
       treeW(red, tid);
     }
     if (tid == 0) {
@@ -1333,19 +1413,19 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, sum, cnt);
+      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
       // half 1 of the centre partials (read in P5 below; the next baseline B writes half 0)
-      unsigned long long* cp1 = a.cpart + 2 * (size_t)gridDim.x;
-      if (tid == 0) { cp1[2 * blockIdx.x] = S; cp1[2 * blockIdx.x + 1] = n; }
-      grid_barrier(st, gen);  // sNA is identical in every CTA: uniform barrier
+      unsigned long long* cp1 = cpart + 2 * (size_t)nb;
+      if (tid == 0) { cp1[2 * lb] = S; cp1[2 * lb + 1] = n; }
+      grid_barrier(st, gen, nb);  // sNA is identical in every CTA: uniform barrier
     }
     PFT_TMARK(4);
     // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
     unsigned long long S5 = 0ull, n5 = 0ull;
-    if (sNA > 0) sum_partials(a.cpart + 2 * (size_t)gridDim.x, gridDim.x, sS, sNw, S5, n5);
+    if (sNA > 0) sum_partials(cpart + 2 * (size_t)nb, nb, sS, sNw, S5, n5);
     if (tid == 0) {
       double Ec = sState[3];
       unsigned nc = sNcBase;
@@ -1366,7 +1446,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       const double f = s_factor(a.beta, Ec);
       const double om1 = __dmul_rn(f, om), v1 = __dmul_rn(f, v);
       const bool stop = stop_now(a.sr, om1, v1, stalls);
-      if (blockIdx.x == 0 && a.trace) {
+      if (lb == 0 && out_rank && a.trace) {
         const int flags = (sNA == 0 ? 1 : 0) | (sState[3] == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0) | (rejected ? 8 : 0) |
                           (stop ? 16 : 0);
         write_trace(a.trace + (size_t)it * PFT_TRACE_DOUBLES, sState[3], sNA, om, v, sP, Ec, om1, v1, flags, nc, N, Ki,
@@ -1379,23 +1459,29 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     PFT_TMARK(5);
     if (sStop) { ++it; break; }  // identical decision in every CTA
   }
-  if (timing && tid == 0 && blockIdx.x == 0)
+  if (timing && tid == 0 && lb == 0)
     printf("pft phase timing (us, %d iterations, %d CTAs): P0 %.1f  B %.1f  P1 %.1f  P2 %.1f (tail %.1f)  P3 %.1f  P4 %.1f  P5 %.1f\n",
-           it, (int)gridDim.x, tph[7] * 1e-3, tph[0] * 1e-3, tph[1] * 1e-3, tph[2] * 1e-3, tph[6] * 1e-3,
+           it, (int)nb, tph[7] * 1e-3, tph[0] * 1e-3, tph[1] * 1e-3, tph[2] * 1e-3, tph[6] * 1e-3,
            tph[3] * 1e-3, tph[4] * 1e-3, tph[5] * 1e-3);
 #undef PFT_TMARK
   // ---- outputs
-  if (blockIdx.x == 0 && tid == 0) {
-    for (int q = 0; q < 12; ++q) { a.T_out[q] = sP[q]; st->P[q] = sP[q]; }
+  if (lb == 0 && tid == 0) {
+    for (int q = 0; q < 12; ++q) st->P[q] = sP[q];
     st->omega = sState[0]; st->v = sState[1]; st->Ec = sState[2]; st->nA = sNA; st->nc = sNc;
     st->iter = it; st->K_last = sKlast; st->stopped = sStop;
-    if (a.trace)
-      for (int r = it; r < a.iters; ++r) write_not_run(a.trace + (size_t)r * PFT_TRACE_DOUBLES);
+    if (G > 1) *(unsigned long long*)(sXbuf[grp] + a.o_xcnt + kMaxFusedRanks * sizeof(unsigned long long)) =
+        xround0 + (unsigned long long)it;  // exchange rounds completed (every CTA read xround0 before P0's barrier)
+    if (out_rank) {
+      for (int q = 0; q < 12; ++q) a.T_out[q] = sP[q];
+      if (a.trace)
+        for (int r = it; r < a.iters; ++r) write_not_run(a.trace + (size_t)r * PFT_TRACE_DOUBLES);
+    }
   }
-  for (int k = sKlast + blockIdx.x * kThreads + tid; k < a.K; k += gridDim.x * kThreads) {
-    a.E_out[k] = 1.0;
-    a.n_out[k] = 0;
-  }
+  if (out_rank)
+    for (int k = sKlast + lb * kThreads + tid; k < a.K; k += nb * kThreads) {
+      a.E_out[k] = 1.0;
+      a.n_out[k] = 0;
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -1403,7 +1489,6 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
                         const pft_track_params* prm, int nranks, TrackLayout* L) {
-  (void)vol;
   if (nparticles < 1) return fail(PFT_ERR_INVALID_ARG, "number of particles/poses must be >= 1");
   if (prm->stride < 1) return fail(PFT_ERR_INVALID_ARG, "stride must be >= 1");
   if (prm->nsched < 0 || prm->nsched > PFT_MAX_SCHED) return fail(PFT_ERR_INVALID_ARG, "nsched must be in [0,%d]", PFT_MAX_SCHED);
@@ -1454,7 +1539,16 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024 + sizeof(unsigned long long) * 148 * 8, 256);
   L->topk_off = off;
   off = align_up(off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)L->nblk_upd + 16 * sizeof(double), 256);
-  L->total = off;
+  L->xch_off = 0;
+  L->xcnt_rel = 0;
+  if (vol && vol->virtual_fused && nranks > 1) {
+    // two halves of G * kloc records, then the counters
+    L->xch_off = off;
+    L->xcnt_rel = align_up(2 * sizeof(PartRec) * (size_t)L->kfull, 256);
+    off = align_up(off + L->xcnt_rel + (kMaxFusedRanks + 1) * sizeof(unsigned long long), 256);
+  }
+  L->region = off;
+  L->total = (vol && vol->virtual_fused && nranks > 1) ? off * (size_t)nranks : off;
   return PFT_OK;
 }
 
@@ -1528,28 +1622,40 @@ static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin
   }
 }
 
-// Persistent single-launch tracker (G = 1): cooperative launch, all CTAs co-resident.
+// Persistent single-launch tracker: cooperative launch, all CTAs co-resident.  G = 1; or G rank
+// groups of CTAs in one launch (fused one-GPU emulation of F2, each group in its own workspace
+// region); or one group per GPU with the peers' exchange buffers attached (pft_comm_p2p_attach).
 template <typename T>
 static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
                                    const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                                    int32_t* n_out, double* trace) {
-  static int grid = 0;
-  if (grid == 0) {
+  static int cap = 0;
+  if (cap == 0) {
     int per_sm = 0, sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kThreads, 0);
-    grid = per_sm * sms;
-    if (grid > 148 * 8) grid = 148 * 8;
-    if (grid < 1) return fail(PFT_ERR_CUDA, "persistent tracker does not fit on the device");
+    cap = per_sm * sms;
+    if (cap > 148 * 8) cap = 148 * 8;
+    if (cap < 1) return fail(PFT_ERR_CUDA, "persistent tracker does not fit on the device");
   }
-  cudaMemsetAsync(c.state(), 0, sizeof(TrackState), c.st);
-  cudaMemsetAsync(c.ws + c.L.work_off, 0, sizeof(unsigned) * (size_t)prm->iters, c.st);
+  pft_volume* vol = c.vol;
+  const bool emul = vol->virtual_fused && vol->nranks > 1;
+  const int G = (emul || vol->p2p) ? vol->nranks : 1;
+  const int nb = emul ? cap / G : cap;
+  if (nb < 1) return fail(PFT_ERR_INVALID_ARG, "%d rank groups do not fit in %d co-resident CTAs", G, cap);
+  const int grid = emul ? nb * G : nb;
+  const size_t region = c.L.region;
+  for (int q = 0; q < (emul ? G : 1); ++q) {
+    char* w = c.ws + (size_t)q * region;
+    cudaMemsetAsync(w + c.L.state_off, 0, sizeof(TrackState), c.st);
+    cudaMemsetAsync(w + c.L.work_off, 0, sizeof(unsigned) * (size_t)prm->iters, c.st);
+  }
   PArgs pa;
-  pa.R = c.vol->base + c.vol->L.r_off;
-  pa.V = c.vol->base + c.vol->L.v_off;
-  pa.mask = (const unsigned long long*)(c.vol->base + c.vol->L.m_off);
-  pa.g = c.vol->g;
+  pa.R = vol->base + vol->L.r_off;
+  pa.V = vol->base + vol->L.v_off;
+  pa.mask = (const unsigned long long*)(vol->base + vol->L.m_off);
+  pa.g = vol->g;
   pa.f = frame_of(c, depth, K);
   pa.sc = c.sched();
   pa.pst = pst;
@@ -1561,20 +1667,43 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
   pa.sr = StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit};
   pa.T_init = T_init;
-  pa.st = c.state();
-  pa.acc = (PartRec*)(c.ws + c.L.acc_local_off);
   pa.E_out = E; pa.n_out = n_out; pa.trace = trace; pa.T_out = T_out;
-  pa.ptab = (double*)(c.ws + c.L.ptab_off);
-  pa.pflag = (int*)(c.ws + c.L.ptab_off + 12 * sizeof(double) * (size_t)Kp);
-  pa.upart = (double*)(c.ws + c.L.part_off);
-  pa.cpart = (unsigned long long*)(c.ws + c.L.cpart_off);
-  pa.work = (unsigned*)(c.ws + c.L.work_off);
   static const bool timing = [] { const char* e = getenv("PFT_PHASE_TIMING"); return e && e[0] == '1'; }();
-  pa.tdone = timing ? (unsigned long long*)(c.ws + c.L.work_off + 1024 * sizeof(unsigned)) : nullptr;
+  pa.tdone = (timing && !emul) ? (unsigned long long*)(c.ws + c.L.work_off + 1024 * sizeof(unsigned)) : nullptr;
   pa.topk = prm->topk;
-  pa.ckey = (unsigned long long*)(c.ws + c.L.topk_off);
-  pa.cidx = (int*)(c.ws + c.L.topk_off + sizeof(unsigned long long) * kTopkMax * (size_t)c.L.nblk_upd);
-  pa.tkout = (double*)(c.ws + c.L.topk_off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)c.L.nblk_upd);
+  pa.ws = c.ws;
+  pa.rank_stride = region;
+  pa.o_state = c.L.state_off;
+  pa.o_acc = c.L.acc_local_off;
+  pa.o_ptab = c.L.ptab_off;
+  pa.o_pflag = c.L.ptab_off + 12 * sizeof(double) * (size_t)Kp;
+  pa.o_upart = c.L.part_off;
+  pa.o_cpart = c.L.cpart_off;
+  pa.o_work = c.L.work_off;
+  pa.o_ckey = c.L.topk_off;
+  pa.o_cidx = c.L.topk_off + sizeof(unsigned long long) * kTopkMax * (size_t)c.L.nblk_upd;
+  pa.o_tkout = c.L.topk_off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)c.L.nblk_upd;
+  pa.G = G;
+  pa.rank = emul ? 0 : (G > 1 ? vol->rank : 0);
+  pa.emul = emul ? 1 : 0;
+  for (int q = 0; q < kMaxFusedRanks; ++q) pa.xbuf[q] = nullptr;
+  pa.o_xcnt = 0;
+  if (emul) {
+    for (int q = 0; q < G; ++q) pa.xbuf[q] = c.ws + (size_t)q * region + c.L.xch_off;
+    pa.o_xcnt = c.L.xcnt_rel;
+    // the counters are monotone across calls (pft.h: F2 exchange); a new workspace starts them at 0
+    if (vol->xws_last != c.ws || vol->xws_total != c.L.total) {
+      for (int q = 0; q < G; ++q)
+        cudaMemsetAsync(pa.xbuf[q] + pa.o_xcnt, 0, (kMaxFusedRanks + 1) * sizeof(unsigned long long), c.st);
+      vol->xws_last = c.ws;
+      vol->xws_total = c.L.total;
+    }
+  } else if (G > 1) {
+    if (Kp > vol->xmax_particles)
+      return fail(PFT_ERR_INVALID_ARG, "%d particles exceed the exchange buffer's %d", Kp, vol->xmax_particles);
+    for (int q = 0; q < G; ++q) pa.xbuf[q] = vol->xbuf[q];
+    pa.o_xcnt = vol->xcnt_off;
+  }
   void* args[] = {&pa};
   cudaError_t e = cudaSuccess;
   PFT_LAUNCH(PFT_PROF_TRACK, c.st,
@@ -1596,7 +1725,7 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
                             const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                             int32_t* n_out, double* trace) {
   const int G = c.vol->nranks, r = c.vol->rank;
-  if (G == 1 && use_persistent() && prm->iters <= 1024)
+  if ((G == 1 || c.vol->virtual_fused || c.vol->p2p) && use_persistent() && prm->iters <= 1024)
     return track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
   const int kloc = c.L.kloc;
   const int k_begin = r * kloc;

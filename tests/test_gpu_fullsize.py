@@ -116,3 +116,22 @@ def test_sequence_Q_512_lockstep():
 def test_sequence_L_1024_fp16_lockstep():
     """Config L: 1024^3 @ 5 mm, tau 2 cm, fp16 values and weights (bit-exact fp16 rounding), K = 4096."""
     _lockstep("L", 3, 4096)
+
+
+def test_sweep_W_k4096_fused_exchange_G8(sweep):
+    """Config W, K = 4096, 10 iterations: the F2 fused exchange emulated with 8 rank groups in one
+    launch (37 CTAs each) equals the 1-rank persistent run bit for bit."""
+    import paper_2509_24236_b200 as pft
+    c, vol, ov = sweep
+    pst = T(c["pst"][:4096].copy())
+    params = TrackParams(iters=10, stride=4)
+    a = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
+    a = {k: a[k].cpu().numpy() for k in ("T", "E", "n", "trace")}
+    v8 = pft.Volume(c["desc"], dev())
+    v8.upload(c["V"], c["W"])
+    v8.comm_init_virtual(8, fused=True)
+    b = v8.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
+    torch.cuda.synchronize()
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(a[k], b[k].cpu().numpy()), k
+    v8.close()

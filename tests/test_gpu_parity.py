@@ -444,3 +444,57 @@ def test_virtual_shards_bit_identical(pft, G):  # noqa: C901
         for k in ("T", "E", "n", "trace"):
             assert np.array_equal(a[k], b[k]), (name, G, k)
         vol.close()
+
+
+def _fused_cases():
+    import dataclasses
+    out = []
+    c = config_single(seed=1)
+    out.append(("single", c, c["pst"], c["params"]))
+    c = config_single(seed=2)
+    out.append(("single_topk", c, c["pst"], dataclasses.replace(c["params"], update_rule=2, topk=32, iters=4)))
+    c = config_tiny(seed=2)
+    out.append(("tiny_sched", c, make_pst(2, 61),
+                dataclasses.replace(TrackParams(iters=7, stride=1, guard=1, update_rule=1), **SCHED_TINY)))
+    c = config_tiny(seed=1)
+    out.append(("tiny_stop", c, c["pst"], TrackParams(iters=8, stride=2, min_search_deg=4.0, min_search_cm=1e9)))
+    return out
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_fused_exchange_bit_identical(pft, G):
+    """F2 fused exchange (include/pft.h pft_comm_init_virtual_fused): G rank groups of CTAs in ONE
+    persistent launch, each evaluating its shard and pushing its per-particle records into every
+    group's exchange buffer, waiting on the same monotone counters the multi-GPU path uses.  Equals
+    the 1-rank run bit for bit (T, every E_k / n_k, every trace row), including a top-k run, a
+    scheduled ragged-K weighted/guarded run (K = 61: empty and ragged shards) and an early stop."""
+    for name, c, pst, params in _fused_cases():
+        ref = gpu_volume(pft, c["desc"], c["V"], c["W"])
+        a = run_track(pft, ref, c["depth"], c["intr"], c["T_init"], pst, params)
+        ref.close()
+        vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+        vol.comm_init_virtual(G, fused=True)
+        ws_bytes = vol.workspace(c["intr"], pst.shape[0], params).numel()
+        b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
+        for k in ("T", "E", "n", "trace"):
+            assert np.array_equal(a[k], b[k]), (name, G, k)
+        # a second call on the same workspace: the exchange counters continue from the stored
+        # round count (no reset handshake) and the results repeat
+        b2 = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
+        for k in ("T", "E", "n", "trace"):
+            assert np.array_equal(a[k], b2[k]), (name, G, k, "second call")
+        assert vol.workspace(c["intr"], pst.shape[0], params).numel() == ws_bytes
+        vol.close()
+
+
+def test_fused_exchange_one_launch(pft):
+    """The fused G-rank emulation is one kernel launch per pft_track call (no per-iteration
+    collective or host round trip)."""
+    c = config_single(seed=1)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    vol.comm_init_virtual(4, fused=True)
+    run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
+    n0 = pft.launch_count()
+    run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
+    assert pft.launch_count() - n0 == 1
+    vol.close()

@@ -127,3 +127,33 @@ def test_shard_ranges_cover_exactly_once():
                 assert (b, n) == shard_range(K, G, r)
                 seen[b:b + n] += 1
             assert np.all(seen == 1)
+
+
+def _handles_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_24236_b200.api import gather_handles
+    mine = bytes((rank * 37 + i) % 256 for i in range(64))
+    q.put((rank, gather_handles(mine)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_handle_gather(world):
+    """Host plumbing of the F2 peer exchange (api.Volume.comm_init_p2p): every rank receives all
+    ranks' 64-byte CUDA IPC handles, concatenated in rank order, over torch.distributed (gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = b"".join(bytes((r * 37 + i) % 256 for i in range(64)) for r in range(world))
+    for r in range(world):
+        assert res[r] == want
