@@ -346,8 +346,8 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
     o[p] = (offx(ix) + offy(iy, g.sy) + offz(iz, g.sz)) & (0u - (uint32_t)ok[p]);
   }
   // in band iff all 8 corners |V| < 1 (reading L3): one bit per cell, precomputed from the
-  // same stored values by the record builder
-  unsigned long long mw[PPT];
+  // same stored values by the record builder; read as the 32-bit half of the brick's word
+  uint32_t mw[PPT];
 #ifdef PFT_DEBUG
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
@@ -365,12 +365,13 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
   const char* rbase = reinterpret_cast<const char*>(R);
 #pragma unroll
   for (int p = 0; p < PPT; ++p)
-    mw[p] = __ldg(reinterpret_cast<const unsigned long long*>(mbase + (size_t)(o[p] >> 6) * 8u));
+    mw[p] = __ldg(reinterpret_cast<const unsigned*>(mbase + (size_t)(o[p] >> 5) * 4u));
   float v[PPT][8];
+  uint32_t inb[PPT];  // 1 iff the evaluation is counted (in range, valid point, in band)
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    ok[p] = ok[p] && ((mw[p] >> (o[p] & 63)) & 1ull);
-    const uint32_t orec = o[p] & (0u - (uint32_t)ok[p]);
+    inb[p] = (mw[p] >> (o[p] & 31u)) & (uint32_t)ok[p];
+    const uint32_t orec = o[p] * inb[p];
     ld_rec(reinterpret_cast<const T*>(rbase + (size_t)orec * (8u * sizeof(T))), v[p]);
   }
 #pragma unroll
@@ -391,8 +392,8 @@ __device__ __forceinline__ void eval_points(const T* __restrict__ R, const unsig
       const float c0 = fmaf(fy[p], c10 - c00, c00), c1 = fmaf(fy[p], c11 - c01, c01);
       val = fmaf(fz[p], c1 - c0, c0);
     }
-    fix += ok[p] ? __float2uint_rn(fabsf(val) * (float)kFixScale) : 0u;
-    cnt += ok[p] ? 1u : 0u;
+    fix += __float2uint_rn(fabsf(val) * (float)kFixScale) * inb[p];
+    cnt += inb[p];
   }
 }
 
