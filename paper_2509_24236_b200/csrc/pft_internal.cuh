@@ -114,7 +114,7 @@ struct TrackState {
   int K_last;          // K_i of the last iteration that ran
   unsigned int ticket_upd, ticket_ctr;
   unsigned long long pmax_bits;  // max |point coordinate| over all sets (persistent path)
-  unsigned int bar_count, bar_gen;  // software grid barrier (persistent path)
+  unsigned long long bar_mono;      // persistent path: grid-barrier arrivals (monotone within a launch)
   double pad[4];
 };
 
