@@ -177,6 +177,9 @@ def run_ours(args):
         step(i, depth_dev[i], tinit_dev[i])
     barrier()
 
+    # the e2e run below replays the same frames from the same map state (integration changes the map)
+    snap = vol.storage.clone()
+
     # ---- device-resident timed region
     idx = list(range(args.warmup, args.warmup + args.steps))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
@@ -211,6 +214,8 @@ def run_ours(args):
     d_buf = torch.empty_like(depth_dev[0])
     t_buf = torch.empty_like(tinit_dev[0])
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
+    vol.storage.copy_(snap)
+    del snap
     barrier()
     for j, i in enumerate(idx):
         flush.zero_()
