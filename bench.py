@@ -211,8 +211,23 @@ def run_ours(args):
     host_depth = [torch.from_numpy(s["depth"]).pin_memory() for s in steps_in]
     host_tinit = [torch.from_numpy(s["T_init"]).pin_memory() for s in steps_in]
     host_T = [torch.empty(3, 4, dtype=torch.float64).pin_memory() for _ in idx]
-    d_buf = torch.empty_like(depth_dev[0])
-    t_buf = torch.empty_like(tinit_dev[0])
+    # double-buffered inputs: frame j+1's H2D runs on a copy stream while frame j computes (a
+    # user's pipeline); every copy lies inside some step's event window (frame 0's inside its own)
+    d_buf = [torch.empty_like(depth_dev[0]) for _ in range(2)]
+    t_buf = [torch.empty_like(tinit_dev[0]) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    used = [torch.cuda.Event() for _ in range(2)]
+    cs = torch.cuda.Stream(device=dev)
+
+    def prefetch(j):
+        i, b = idx[j], j & 1
+        with torch.cuda.stream(cs):
+            if j >= 2:
+                cs.wait_event(used[b])
+            d_buf[b].copy_(host_depth[i], non_blocking=True)
+            t_buf[b].copy_(host_tinit[i], non_blocking=True)
+            ready[b].record(cs)
+
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
     vol.storage.copy_(snap)
     del snap
@@ -220,9 +235,15 @@ def run_ours(args):
     for j, i in enumerate(idx):
         flush.zero_()
         ev2[j][0].record(stream)
-        d_buf.copy_(host_depth[i], non_blocking=True)
-        t_buf.copy_(host_tinit[i], non_blocking=True)
-        step(i, d_buf, t_buf)
+        if j == 0:
+            cs.wait_event(ev2[0][0])
+            prefetch(0)
+        b = j & 1
+        stream.wait_event(ready[b])
+        if j + 1 < len(idx):
+            prefetch(j + 1)
+        step(i, d_buf[b], t_buf[b])
+        used[b].record(stream)
         host_T[j].copy_(out["T"], non_blocking=True)
         ev2[j][1].record(stream)
     barrier()
