@@ -63,7 +63,7 @@ typedef enum { PFT_UPDATE_MEAN = 0, PFT_UPDATE_WEIGHTED = 1, PFT_UPDATE_TOPK = 2
 #define PFT_MAX_SCHED 4
 
 typedef struct {
-  int32_t nx, ny, nz;   /* voxels per axis, each >= 2                                        */
+  int32_t nx, ny, nz;   /* voxels per axis, each in [2, 4096]                                */
   double voxel_m;       /* voxel edge (m), > 0                                               */
   double origin_m[3];   /* min corner of the grid (m)                                        */
   double trunc_m;       /* tau (m), >= 2 * voxel_m                              */

@@ -33,27 +33,38 @@ template <typename T> __device__ __forceinline__ bool same_bits(T a, T b);
 template <> __device__ __forceinline__ bool same_bits<float>(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
 template <> __device__ __forceinline__ bool same_bits<__half>(__half a, __half b) { return __half_as_ushort(a) == __half_as_ushort(b); }
 
+// Exact int -> double without the conversion pipe (XU): 2^52 + i has i in its low mantissa bits.
+__device__ __forceinline__ double i2d(int i) {  // 0 <= i < 2^31
+  return __dsub_rn(__hiloint2double(0x43300000, i), 4503599627370496.0);
+}
+// floor(x) as an int for |x| < 2^30 (exact; no FRND): x + 1.5*2^52 rounded toward -inf holds
+// floor(x) in its low word.
+__device__ __forceinline__ int floor_lo(double x) { return __double2loint(__dadd_rd(x, 6755399441055744.0)); }
+
 // Returns true iff the stored value V changed (its cell records must then be refreshed).
 template <typename T>
 __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
                                            const double* T_, int i, int j, int k, T* __restrict__ V,
                                            T* __restrict__ W, uint32_t o) {
-  const double gw0 = __dadd_rn(g.ox, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
-  const double gw1 = __dadd_rn(g.oy, __dmul_rn(g.voxel, __dadd_rn((double)j, 0.5)));
-  const double gw2 = __dadd_rn(g.oz, __dmul_rn(g.voxel, __dadd_rn((double)k, 0.5)));
+  const double gw0 = __dadd_rn(g.ox, __dmul_rn(g.voxel, __dadd_rn(i2d(i), 0.5)));
+  const double gw1 = __dadd_rn(g.oy, __dmul_rn(g.voxel, __dadd_rn(i2d(j), 0.5)));
+  const double gw2 = __dadd_rn(g.oz, __dmul_rn(g.voxel, __dadd_rn(i2d(k), 0.5)));
   const double d0 = __dsub_rn(gw0, T_[3]), d1 = __dsub_rn(gw1, T_[7]), d2 = __dsub_rn(gw2, T_[11]);
   const double z = __dadd_rn(__dadd_rn(__dmul_rn(T_[2], d0), __dmul_rn(T_[6], d1)), __dmul_rn(T_[10], d2));
   if (!(z > 0.0)) return false;
   const double x = __dadd_rn(__dadd_rn(__dmul_rn(T_[0], d0), __dmul_rn(T_[4], d1)), __dmul_rn(T_[8], d2));
   const double y = __dadd_rn(__dadd_rn(__dmul_rn(T_[1], d0), __dmul_rn(T_[5], d1)), __dmul_rn(T_[9], d2));
-  const double u = __dadd_rn(__ddiv_rn(__dmul_rn(K.fx, x), z), K.cx);
-  const double uf = floor(__dadd_rn(u, 0.5));
-  if (!(uf >= 0.0 && uf < (double)K.W)) return false;
-  const double v = __dadd_rn(__ddiv_rn(__dmul_rn(K.fy, y), z), K.cy);
-  const double vf = floor(__dadd_rn(v, 0.5));
-  if (!(vf >= 0.0 && vf < (double)K.H)) return false;
-  const uint16_t raw = __ldg(depth + (size_t)vf * K.W + (size_t)uf);
-  const double d = __dmul_rn((double)raw, K.unit);
+  // pixel = floor(u + 1/2): out of [0, W) also for |u + 1/2| >= 2^30 and NaN
+  const double u2 = __dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(K.fx, x), z), K.cx), 0.5);
+  if (!(fabs(u2) < 1073741824.0)) return false;
+  const int ui = floor_lo(u2);
+  if ((unsigned)ui >= (unsigned)K.W) return false;
+  const double v2 = __dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(K.fy, y), z), K.cy), 0.5);
+  if (!(fabs(v2) < 1073741824.0)) return false;
+  const int vi = floor_lo(v2);
+  if ((unsigned)vi >= (unsigned)K.H) return false;
+  const uint16_t raw = __ldg(depth + (size_t)vi * K.W + (size_t)ui);
+  const double d = __dmul_rn(i2d((int)raw), K.unit);
   if (raw == 0 || !(d < g.max_depth)) return false;
   const double sdf = __dsub_rn(d, z);
   if (!(sdf > -g.trunc)) return false;
@@ -155,6 +166,13 @@ __device__ __forceinline__ bool box_visible(const Geom& g, const Intr& K, const 
   return zn - 1e-3f < dmax + (float)g.trunc;
 }
 
+// Kept-brick list entries carry the brick coordinates packed 10:10:10 bits (grids up to 4096
+// voxels per axis, checked at volume creation), so the sweep decodes them with shifts instead of
+// two runtime integer divisions per thread.
+__device__ __forceinline__ uint32_t pack_brick(int bx, int by, int bz) {
+  return ((uint32_t)bz << 20) | ((uint32_t)by << 10) | (uint32_t)bx;
+}
+
 __device__ __forceinline__ void append_warp(bool keep, uint32_t v, uint32_t* __restrict__ list,
                                             uint32_t* __restrict__ count) {
   const unsigned ball = __ballot_sync(0xffffffffu, keep);
@@ -206,7 +224,7 @@ __global__ __launch_bounds__(512) void k_cull_bricks(Geom g, Intr K, const doubl
     if (bx < g.nbx && by < g.nby && bz < g.nbz)
       keep = box_visible(g, K, Tdev, tiles, ntx, g.ox + g.voxel * (4.0 * bx + 2.0), g.oy + g.voxel * (4.0 * by + 2.0),
                          g.oz + g.voxel * (4.0 * bz + 2.0), (float)(1.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
-    append_warp(keep, ((uint32_t)bz * g.nby + (uint32_t)by) * g.nbx + (uint32_t)bx, list, count);
+    append_warp(keep, pack_brick(bx, by, bz), list, count);
   }
 }
 
@@ -223,10 +241,9 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
   const uint32_t n = *count;
   const uint32_t w = threadIdx.x & 63;
   for (uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6); li < n; li += gridDim.x * 4) {
-    const uint32_t b = list[li];
-    const int bx = (int)(b % (uint32_t)g.nbx);
-    const uint32_t r = b / (uint32_t)g.nbx;
-    const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
+    const uint32_t e = list[li];
+    const int bx = (int)(e & 1023u), by = (int)((e >> 10) & 1023u), bz = (int)(e >> 20);
+    const uint32_t b = ((uint32_t)bz * g.nby + (uint32_t)by) * g.nbx + (uint32_t)bx;
     const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
     bool changed = false;
     if (i < g.nx && j < g.ny && k < g.nz) changed = fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, b * 64u + w);

@@ -15,6 +15,8 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static pft_status check_desc(const pft_volume_desc* d) {
   if (!d) return fail(PFT_ERR_INVALID_ARG, "desc is NULL");
   if (d->nx < 2 || d->ny < 2 || d->nz < 2) return fail(PFT_ERR_INVALID_ARG, "dims must be >= 2 (got %d %d %d)", d->nx, d->ny, d->nz);
+  if (d->nx > 4096 || d->ny > 4096 || d->nz > 4096)
+    return fail(PFT_ERR_INVALID_ARG, "dims must be <= 4096 (got %d %d %d)", d->nx, d->ny, d->nz);
   if (!(d->voxel_m > 0.0)) return fail(PFT_ERR_INVALID_ARG, "voxel_m must be > 0");
   if (!(d->trunc_m >= 2.0 * d->voxel_m)) return fail(PFT_ERR_INVALID_ARG, "trunc_m must be >= 2*voxel_m (SPEC.md:219)");
   if (!(d->max_weight >= 1.0)) return fail(PFT_ERR_INVALID_ARG, "max_weight must be >= 1");

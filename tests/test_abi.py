@@ -63,7 +63,7 @@ def test_volume_bytes_and_validation(pft):
     n16 = C.c_size_t()
     assert L.pft_volume_bytes(C.byref(_desc(pft, storage=1)), C.byref(n16)) == 0
     assert n16.value < n.value
-    bad = [dict(nx=1), dict(voxel_m=0.0), dict(trunc_m=0.03), dict(max_weight=0.5), dict(storage=7),
+    bad = [dict(nx=1), dict(nz=4097), dict(voxel_m=0.0), dict(trunc_m=0.03), dict(max_weight=0.5), dict(storage=7),
            dict(max_depth_m=0.0)]
     for b in bad:
         assert L.pft_volume_bytes(C.byref(_desc(pft, **b)), C.byref(n)) == -1, b
