@@ -130,40 +130,65 @@ __global__ void k_depth_tiles(Intr K, double max_depth, const uint16_t* __restri
 // (all z_c <= 0, projection misses the image, or every pixel it can project to is invalid or has
 // d + tau <= z_c).  fp32 with margins (1 mm, 2 px) far above fp32 rounding at room scale.  Boxes
 // straddling the camera plane, or covering more than max_tiles depth tiles, are kept.
-__device__ __forceinline__ bool box_visible(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
-                                            const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
-                                            double czw, float rad, int max_tiles) {
+struct Footprint {
+  int verdict;  // 0 reject, 1 keep, 2 decided by the max depth over tiles [t0x,t1x] x [t0y,t1y] of lvl
+  const uint32_t* lvl;
+  int stride, t0x, t1x, t0y, t1y;
+  float zn;
+};
+
+__device__ __forceinline__ Footprint box_footprint(const Intr& K, const double* __restrict__ Tdev,
+                                                   const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
+                                                   double czw, float rad, int max_tiles) {
+  Footprint f;
+  f.verdict = 0;
   const float cwx = (float)(cxw - Tdev[3]), cwy = (float)(cyw - Tdev[7]), cwz = (float)(czw - Tdev[11]);
   const float x = (float)Tdev[0] * cwx + (float)Tdev[4] * cwy + (float)Tdev[8] * cwz;
   const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
   const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
-  if (!(z + rad > 0.f)) return false;
-  if (z - rad <= 1e-3f) return true;  // straddles the camera plane: no projection bound
+  if (!(z + rad > 0.f)) return f;
+  f.verdict = 1;
+  if (z - rad <= 1e-3f) return f;  // straddles the camera plane: no projection bound
   const float zn = z - rad, zf = z + rad;
   const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
   const float u0 = fx * fminf((x - rad) / zn, (x - rad) / zf) + cx - 2.f;
   const float u1 = fx * fmaxf((x + rad) / zn, (x + rad) / zf) + cx + 2.f;
   const float v0 = fy * fminf((y - rad) / zn, (y - rad) / zf) + cy - 2.f;
   const float v1 = fy * fmaxf((y + rad) / zn, (y + rad) / zf) + cy + 2.f;
-  if (!(u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H)) return false;
+  f.verdict = 0;
+  if (!(u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H)) return f;
   const int pu0 = max(0, (int)floorf(u0 + 0.5f)), pu1 = min(K.W - 1, (int)floorf(u1 + 0.5f));
   const int pv0 = max(0, (int)floorf(v0 + 0.5f)), pv1 = min(K.H - 1, (int)floorf(v1 + 0.5f));
-  int t0x = pu0 / kTile, t1x = pu1 / kTile, t0y = pv0 / kTile, t1y = pv1 / kTile;
-  const uint32_t* lvl = tiles;
-  int stride = ntx;
-  if ((t1x - t0x + 1) * (t1y - t0y + 1) > 64) {  // large footprint: the coarse (8x8-tile) level
+  f.t0x = pu0 / kTile; f.t1x = pu1 / kTile; f.t0y = pv0 / kTile; f.t1y = pv1 / kTile;
+  f.lvl = tiles;
+  f.stride = ntx;
+  f.zn = zn;
+  f.verdict = 2;
+  if ((f.t1x - f.t0x + 1) * (f.t1y - f.t0y + 1) > 64) {  // large footprint: the coarse (8x8-tile) level
     const int nty_f = (K.H + kTile - 1) / kTile;
-    lvl = tiles + ntx * nty_f;
-    stride = (ntx + 7) >> 3;
-    t0x >>= 3; t1x >>= 3; t0y >>= 3; t1y >>= 3;
-    if ((t1x - t0x + 1) * (t1y - t0y + 1) > max_tiles) return true;
+    f.lvl = tiles + ntx * nty_f;
+    f.stride = (ntx + 7) >> 3;
+    f.t0x >>= 3; f.t1x >>= 3; f.t0y >>= 3; f.t1y >>= 3;
+    if ((f.t1x - f.t0x + 1) * (f.t1y - f.t0y + 1) > max_tiles) f.verdict = 1;
   }
-  uint32_t m = 0;
-  for (int ty = t0y; ty <= t1y; ++ty)
-    for (int tx = t0x; tx <= t1x; ++tx) m = max(m, __ldg(lvl + ty * stride + tx));
+  return f;
+}
+
+__device__ __forceinline__ bool footprint_keep(const Geom& g, const Intr& K, const Footprint& f, uint32_t m) {
   if (m == 0) return false;
   const float dmax = (float)((double)m * K.unit);
-  return zn - 1e-3f < dmax + (float)g.trunc;
+  return f.zn - 1e-3f < dmax + (float)g.trunc;
+}
+
+__device__ __forceinline__ bool box_visible(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
+                                            const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
+                                            double czw, float rad, int max_tiles) {
+  const Footprint f = box_footprint(K, Tdev, tiles, ntx, cxw, cyw, czw, rad, max_tiles);
+  if (f.verdict != 2) return f.verdict == 1;
+  uint32_t m = 0;
+  for (int ty = f.t0y; ty <= f.t1y; ++ty)
+    for (int tx = f.t0x; tx <= f.t1x; ++tx) m = max(m, __ldg(f.lvl + ty * f.stride + tx));
+  return footprint_keep(g, K, f, m);
 }
 
 // Kept-brick list entries carry the brick coordinates packed 10:10:10 bits (grids up to 4096
@@ -187,23 +212,30 @@ __device__ __forceinline__ void append_warp(bool keep, uint32_t v, uint32_t* __r
 
 constexpr int kSuper = 8;  // super-brick = 8^3 bricks = 32^3 voxels
 
-// Level 1: one thread per super-brick.
+// Level 1: one warp per super-brick; the lanes share the footprint's tile loads.
 __global__ void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev, const uint32_t* __restrict__ tiles,
                              int ntx, int nsx, int nsy, int nsz, uint32_t* __restrict__ slist,
                              uint32_t* __restrict__ scount) {
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
-  const uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false;
-  if (sb < ns) {
-    const int sx = (int)(sb % (uint32_t)nsx);
-    const uint32_t r = sb / (uint32_t)nsx;
-    const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
-    // voxel-centre box of the super-brick: voxels [32 s, 32 s + 31] per axis
-    const double h = 16.0;
-    keep = box_visible(g, K, Tdev, tiles, ntx, g.ox + g.voxel * (32.0 * sx + h), g.oy + g.voxel * (32.0 * sy + h),
-                       g.oz + g.voxel * (32.0 * sz + h), (float)(15.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
+  const uint32_t sb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  if (sb >= ns) return;
+  const int sx = (int)(sb % (uint32_t)nsx);
+  const uint32_t r = sb / (uint32_t)nsx;
+  const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
+  // voxel-centre box of the super-brick: voxels [32 s, 32 s + 31] per axis
+  const double h = 16.0;
+  const Footprint f = box_footprint(K, Tdev, tiles, ntx, g.ox + g.voxel * (32.0 * sx + h), g.oy + g.voxel * (32.0 * sy + h),
+                                    g.oz + g.voxel * (32.0 * sz + h), (float)(15.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
+  bool keep = f.verdict == 1;
+  if (f.verdict == 2) {
+    const int nx = f.t1x - f.t0x + 1, nt = nx * (f.t1y - f.t0y + 1);
+    uint32_t m = 0;
+    for (int t = lane; t < nt; t += 32) m = max(m, __ldg(f.lvl + (f.t0y + t / nx) * f.stride + f.t0x + t % nx));
+    for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
+    keep = footprint_keep(g, K, f, m);
   }
-  append_warp(keep, sb, slist, scount);
+  if (lane == 0 && keep) slist[atomicAdd(scount, 1u)] = sb;
 }
 
 // Level 2: the 512 bricks of every surviving super-brick (one CTA of 512 threads per super-brick).
@@ -298,7 +330,7 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
   uint32_t* slist = (uint32_t*)(vol->base + vol->L.slist_off);
   uint32_t* scount = (uint32_t*)(vol->base + vol->L.scratch_off + 192);
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, nsz, slist, scount));
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns * 32 + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, nsz, slist, scount));
   PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<148 * 4, 512, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, slist, scount, list, count));
   const int grid = 148 * 8;
   if (vol->esize == 4)
