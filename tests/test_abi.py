@@ -110,6 +110,21 @@ def test_create_workspace_and_argument_errors(pft):
     assert L.pft_track(h, dummy, C.byref(badK), dummy, dummy, 16, C.byref(p), dummy, 1 << 30, dummy, dummy, dummy,
                        nul, nul) == -1
     assert L.pft_integrate(h, nul, C.byref(K), dummy, nul) == -1
+    # F2 exchange: argument and state validation happens before any device call
+    hbuf = (C.c_uint8 * 64)()
+    assert L.pft_comm_p2p_init(nul, 2, 0, 1024, hbuf) == -1
+    assert L.pft_comm_p2p_init(h, 1, 0, 1024, hbuf) == -1          # needs >= 2 ranks
+    assert L.pft_comm_p2p_init(h, 9, 0, 1024, hbuf) == -1          # <= PFT_MAX_FUSED_RANKS
+    assert L.pft_comm_p2p_init(h, 2, 2, 1024, hbuf) == -1          # rank out of range
+    assert L.pft_comm_p2p_init(h, 2, 0, 0, hbuf) == -1             # max_particles >= 1
+    assert L.pft_comm_p2p_attach(h, hbuf) == -7                    # init not called
+    assert L.pft_comm_init_virtual_fused(h, 0) == -1
+    assert L.pft_comm_init_virtual_fused(h, 9) == -1
+    assert L.pft_comm_init_virtual_fused(h, 4) == 0
+    ws8 = C.c_size_t()
+    assert L.pft_track_workspace_bytes(h, C.byref(K), 1024, C.byref(p), C.byref(ws8)) == 0
+    assert ws8.value >= 4 * ws.value                               # one region per emulated rank
+    assert L.pft_comm_init_virtual(h, 1) == 0
     assert L.pft_volume_destroy(h) == 0
 
 
