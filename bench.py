@@ -148,10 +148,15 @@ def run_ours(args):
     vol.reset()
     for t, d in enumerate(map_depth):
         vol.integrate(torch.from_numpy(d).to(dev), intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
+    exchange = args.exchange
     if world > 1:
-        if args.exchange == "p2p":
-            vol.comm_init_p2p(K)
-        else:
+        if exchange == "p2p":
+            try:
+                vol.comm_init_p2p(K)
+            except Exception as e:  # e.g. GPUs without peer access: fall back to the NCCL path
+                print(f"bench: P2P exchange unavailable ({e}); using ncclAllGather", file=sys.stderr)
+                exchange = "nccl"
+        if exchange == "nccl":
             vol.comm_init()
     pst = torch.from_numpy(seq.pst).to(dev)
     depth_dev = [torch.from_numpy(s["depth"]).to(dev) for s in steps_in]
@@ -383,7 +388,7 @@ def run_ours(args):
                                "track + integrate", "particles": K, "points_per_frame": statistics.mean(n_valid),
                    "iters": ITERS, "volume": "512^3 fp32", "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"particles sharded x{world}, volume replicated"
-                   + (f", {args.exchange} exchange" if world > 1 else "")},
+                   + (f", {exchange} exchange" if world > 1 else "")},
         "frame_ms": {"median": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
                      "max": max(per_step)},
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
