@@ -150,12 +150,10 @@ def run_ours(args):
         vol.integrate(torch.from_numpy(d).to(dev), intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
     exchange = args.exchange
     if world > 1:
-        if exchange == "p2p":
-            try:
-                vol.comm_init_p2p(K)
-            except Exception as e:  # e.g. GPUs without peer access: fall back to the NCCL path
-                print(f"bench: P2P exchange unavailable ({e}); using ncclAllGather", file=sys.stderr)
-                exchange = "nccl"
+        if exchange == "p2p" and not vol.comm_init_p2p(K):
+            # e.g. GPUs without peer access: every rank detached; fall back to the NCCL path
+            print("bench: P2P exchange unavailable on some rank; using ncclAllGather", file=sys.stderr)
+            exchange = "nccl"
         if exchange == "nccl":
             vol.comm_init()
     pst = torch.from_numpy(seq.pst).to(dev)

@@ -258,6 +258,10 @@ pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks,
 pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int32_t max_particles,
                              uint8_t handle_out[PFT_IPC_HANDLE_BYTES]);
 pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles);
+/* Undoes pft_comm_p2p_init/attach on this rank (closes the peers' mappings, frees the buffer);
+ * the volume is then single-rank again (or keeps an attached NCCL communicator).  For a job
+ * whose ranks could not all attach: every rank detaches and falls back to pft_comm_init. */
+pft_status pft_comm_p2p_detach(pft_volume* vol);
 
 /* ---------------------------------------------------------------- instrumentation */
 

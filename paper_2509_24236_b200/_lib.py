@@ -22,7 +22,7 @@ EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_vol
            "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_extract_surface",
            "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
            "pft_comm_init", "pft_comm_init_virtual", "pft_comm_init_virtual_fused", "pft_comm_p2p_init",
-           "pft_comm_p2p_attach", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
+           "pft_comm_p2p_attach", "pft_comm_p2p_detach", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
 PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records", "track"]
 
@@ -86,6 +86,7 @@ def lib():
         "pft_comm_init_virtual_fused": [P, I32],
         "pft_comm_p2p_init": [P, I32, I32, I32, P],
         "pft_comm_p2p_attach": [P, P],
+        "pft_comm_p2p_detach": [P],
         "pft_profile_start": [],
         "pft_profile_stop": [P, P],
     }

@@ -199,17 +199,27 @@ class Volume:
 
     def comm_init_p2p(self, max_particles, group=None):
         """F2 fused exchange over NVLink peer memory: allocate this rank's exchange buffer, gather
-        every rank's CUDA IPC handle over torch.distributed `group`, open the peers', barrier."""
+        every rank's CUDA IPC handle over torch.distributed `group`, open the peers'.  All ranks
+        agree on the outcome (an all-reduce of a success flag): returns True when every rank is
+        attached; otherwise every rank has detached again and False is returned (use comm_init)."""
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         h = (C.c_uint8 * IPC_HANDLE_BYTES)()
-        check(lib().pft_comm_p2p_init(self.handle, world, rank, int(max_particles), h))
+        ok = lib().pft_comm_p2p_init(self.handle, world, rank, int(max_particles), h) == 0
         handles = gather_handles(bytes(h), group)
-        raw = (C.c_uint8 * (IPC_HANDLE_BYTES * world))(*handles)
-        check(lib().pft_comm_p2p_attach(self.handle, raw))
-        dist.barrier(group=group)
+        if ok:
+            raw = (C.c_uint8 * (IPC_HANDLE_BYTES * world))(*handles)
+            ok = lib().pft_comm_p2p_attach(self.handle, raw) == 0
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32)
+        if dist.get_backend(group) == "nccl":
+            flag = flag.to(self.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) != 1:
+            check(lib().pft_comm_p2p_detach(self.handle))
+            return False
         self.nranks, self.rank = world, rank
         self._ws = {}
+        return True
 
     def close(self):
         if getattr(self, "handle", None):

@@ -260,6 +260,21 @@ pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int3
   return PFT_OK;
 }
 
+pft_status pft_comm_p2p_detach(pft_volume* vol) {
+  if (!vol) return fail(PFT_ERR_INVALID_ARG, "vol is NULL");
+  if (vol->p2p)
+    for (int q = 0; q < vol->nranks; ++q)
+      if (q != vol->rank && vol->xbuf[q]) cudaIpcCloseMemHandle(vol->xbuf[q]);
+  for (int q = 0; q < PFT_MAX_FUSED_RANKS; ++q) vol->xbuf[q] = nullptr;
+  vol->p2p = 0;
+  if (vol->xown) cudaFree(vol->xown);
+  vol->xown = nullptr;
+  vol->xbytes = vol->xcnt_off = 0;
+  vol->xmax_particles = 0;
+  if (!vol->nccl_comm) { vol->nranks = 1; vol->rank = 0; }
+  return PFT_OK;
+}
+
 pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles) {
   if (!vol || !handles) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
   if (!vol->xown) return fail(PFT_ERR_STATE, "pft_comm_p2p_init was not called");

@@ -118,6 +118,7 @@ def test_create_workspace_and_argument_errors(pft):
     assert L.pft_comm_p2p_init(h, 2, 2, 1024, hbuf) == -1          # rank out of range
     assert L.pft_comm_p2p_init(h, 2, 0, 0, hbuf) == -1             # max_particles >= 1
     assert L.pft_comm_p2p_attach(h, hbuf) == -7                    # init not called
+    assert L.pft_comm_p2p_detach(h) == 0 and L.pft_comm_p2p_detach(nul) == -1
     assert L.pft_comm_init_virtual_fused(h, 0) == -1
     assert L.pft_comm_init_virtual_fused(h, 9) == -1
     assert L.pft_comm_init_virtual_fused(h, 4) == 0

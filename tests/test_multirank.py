@@ -157,3 +157,45 @@ def test_p2p_handle_gather(world):
     want = b"".join(bytes((r * 37 + i) % 256 for i in range(64)) for r in range(world))
     for r in range(world):
         assert res[r] == want
+
+
+def _p2p_consensus_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import ctypes as C
+    import types
+    import paper_2509_24236_b200 as pft
+    from paper_2509_24236_b200 import api
+    from synth.configs import config_tiny
+    L = pft.lib()
+    d = api.make_desc(config_tiny(seed=1)["desc"])
+    n = C.c_size_t()
+    L.pft_volume_bytes(C.byref(d), C.byref(n))
+    h = C.c_void_p()
+    assert L.pft_volume_create(C.byref(d), C.c_void_p(1 << 40), n.value, C.byref(h)) == 0  # never dereferenced
+    fake = types.SimpleNamespace(handle=h, device=torch.device("cpu"), nranks=1, rank=0, _ws={})
+    # no GPU here: pft_comm_p2p_init fails on every rank (cudaMalloc), the ranks agree, all detach
+    ok = api.Volume.comm_init_p2p(fake, 64)
+    q.put((rank, ok, fake.nranks))
+    L.pft_volume_destroy(h)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_init_consensus_falls_back_together():
+    """Volume.comm_init_p2p: when any rank cannot attach, every rank detaches and reports False
+    (bench.py then uses the NCCL path on all ranks) -- no rank is left waiting on peers."""
+    if torch.cuda.is_available():
+        pytest.skip("exercises the failure path (no device memory)")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_consensus_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (ok, nr)) for r, ok, nr in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: (False, 1), 1: (False, 1)}
