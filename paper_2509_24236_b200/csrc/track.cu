@@ -955,6 +955,7 @@ struct PArgs {
   int G, rank, emul;
   char* xbuf[kMaxFusedRanks];
   size_t o_xcnt;
+  size_t xhalf;  // records per exchange half: fixed per buffer (a peer may still read the previous call's half)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -1305,7 +1306,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     // rank signals each peer once and every CTA waits until all G shards of the round arrived.
     const PartRec* recs = acc;
     if (G > 1) {
-      const size_t half = (size_t)((xround0 + (unsigned long long)it) & 1ull) * (size_t)G * kloc;  // global round parity
+      const size_t half = (size_t)((xround0 + (unsigned long long)it) & 1ull) * a.xhalf;  // global round parity
       for (int j = lb * kThreads + tid; j < Ks; j += nb * kThreads) {
         const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2*>(acc + j));  // (S, n | pad)
         for (int q = 0; q < G; ++q) __stcg(reinterpret_cast<ulonglong2*>((PartRec*)sXbuf[q] + half + kb + j), r);
@@ -1687,9 +1688,11 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.emul = emul ? 1 : 0;
   for (int q = 0; q < kMaxFusedRanks; ++q) pa.xbuf[q] = nullptr;
   pa.o_xcnt = 0;
+  pa.xhalf = 0;
   if (emul) {
     for (int q = 0; q < G; ++q) pa.xbuf[q] = c.ws + (size_t)q * region + c.L.xch_off;
     pa.o_xcnt = c.L.xcnt_rel;
+    pa.xhalf = (size_t)c.L.kfull;  // emulation: one launch at a time, so a per-call stride is safe
     // the counters are monotone across calls (pft.h: F2 exchange); a new workspace starts them at 0
     if (vol->xws_last != c.ws || vol->xws_total != c.L.total) {
       for (int q = 0; q < G; ++q)
@@ -1702,6 +1705,7 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
       return fail(PFT_ERR_INVALID_ARG, "%d particles exceed the exchange buffer's %d", Kp, vol->xmax_particles);
     for (int q = 0; q < G; ++q) pa.xbuf[q] = vol->xbuf[q];
     pa.o_xcnt = vol->xcnt_off;
+    pa.xhalf = (size_t)G * (size_t)((vol->xmax_particles + G - 1) / G);
   }
   void* args[] = {&pa};
   cudaError_t e = cudaSuccess;

@@ -17,24 +17,30 @@ import pytest
 
 
 class _Rank:
-    def __init__(self, G, kloc):
-        self.rec = [[None] * (G * kloc) for _ in range(2)]
+    def __init__(self, G, nrec):
+        self.rec = [None] * nrec  # one buffer: half h occupies [h * stride, (h + 1) * stride)
         self.cnt = [0] * G
         self.xround = 0
         self.lock = threading.Lock()
 
 
-def _run(G, K, calls, delay, global_parity=True, timeout=5.0):
-    """calls: list of executed-iteration counts per call (identical on every rank, as the stop
-    decision is).  delay(rank, call, it, phase) -> seconds.  Returns the list of violations."""
-    kloc = -(-K // G)
-    ranks = [_Rank(G, kloc) for _ in range(G)]
+def _run(G, K, calls, delay, global_parity=True, fixed_stride=True, timeout=5.0):
+    """calls: executed-iteration counts per call, or (count, K_call) pairs (identical on every
+    rank, as the stop decision is).  The exchange buffer holds 2 halves of G*ceil(K/G) records
+    (K = the largest K_call); with fixed_stride=False a call uses its own G*ceil(K_call/G) stride.
+    delay(rank, call, it, phase) -> seconds.  Returns the list of violations."""
+    calls = [c if isinstance(c, tuple) else (c, K) for c in calls]
+    kmax = max(kc for _, kc in calls)
+    stride_max = G * -(-kmax // G)
+    ranks = [_Rank(G, 2 * stride_max) for _ in range(G)]
     errors = []
 
     def worker(r):
-        kb = r * kloc
-        ks = max(0, min(K, kb + kloc) - kb)
-        for ci, n_exec in enumerate(calls):
+        for ci, (n_exec, Kc) in enumerate(calls):
+            kloc = -(-Kc // G)
+            stride = stride_max if fixed_stride else G * kloc
+            kb = r * kloc
+            ks = max(0, min(Kc, kb + kloc) - kb)
             x0 = ranks[r].xround
             for it in range(n_exec):
                 R = x0 + it
@@ -42,7 +48,7 @@ def _run(G, K, calls, delay, global_parity=True, timeout=5.0):
                 half = (R & 1) if global_parity else (it & 1)
                 for q in range(G):
                     for j in range(ks):
-                        ranks[q].rec[half][kb + j] = (R, r, j)
+                        ranks[q].rec[half * stride + kb + j] = (R, r, j)
                 for q in range(G):
                     with ranks[q].lock:
                         ranks[q].cnt[r] += 1
@@ -52,11 +58,11 @@ def _run(G, K, calls, delay, global_parity=True, timeout=5.0):
                         errors.append(("timeout", r, ci, it))
                         return
                     time.sleep(1e-4)
-                time.sleep(delay(r, ci, it, "p3"))
                 for src in range(G):
                     sb = src * kloc
-                    for j in range(max(0, min(K, sb + kloc) - sb)):
-                        got = ranks[r].rec[half][sb + j]
+                    for j in range(max(0, min(Kc, sb + kloc) - sb)):
+                        time.sleep(delay(r, ci, it, "p3") / max(1, Kc))
+                        got = ranks[r].rec[half * stride + sb + j]
                         if got != (R, src, j):
                             errors.append(("stale", r, ci, it, sb + j, got))
             ranks[r].xround = x0 + n_exec
@@ -94,4 +100,16 @@ def test_protocol_model_detects_per_call_parity():
     def delay(r, ci, it, ph):
         return 0.2 if (r == 1 and ci == 0 and ph == "p3") else 0.0
     errs = _run(2, 16, [1, 2], delay, global_parity=False)
+    assert any(e[0] == "stale" for e in errs)
+
+
+def test_protocol_varying_k_needs_fixed_stride():
+    """Consecutive calls with different K (e.g. a schedule-length change): the half stride is fixed
+    per buffer (include/pft.h, bench K), so round R's half never overlaps the other half a slow
+    peer may still be reading; a per-call stride (G*ceil(K_call/G)) overlaps it."""
+    def delay(r, ci, it, ph):
+        return 0.3 if (r == 1 and ci == 0 and ph == "p3") else 0.0
+    calls = [(1, 64), (2, 16)]
+    assert _run(2, 64, calls, delay) == []
+    errs = _run(2, 64, calls, delay, fixed_stride=False)
     assert any(e[0] == "stale" for e in errs)
