@@ -41,8 +41,9 @@ __device__ __forceinline__ void rodrigues(const double r[3], double dR[9]) {
   } else {
     double s, c;
     sincos(th, &s, &c);
-    A = s / th;
-    B = (1.0 - c) / (th * th);
+    const double ith = 1.0 / th;
+    A = s * ith;
+    B = (1.0 - c) * ith * ith;
   }
   const double K[9] = {0.0, -r[2], r[1], r[2], 0.0, -r[0], -r[1], r[0], 0.0};
 #pragma unroll
@@ -94,11 +95,12 @@ __device__ __forceinline__ void apply_delta(const double dR[9], const double u[3
 __device__ __forceinline__ bool fold_pose(const double T[12], const Geom& g, double m[12]) {
   const double o[3] = {g.ox, g.oy, g.oz};
   bool ok = true;
+  const double iv = 1.0 / g.voxel;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) m[4 * i + j] = T[4 * i + j] / g.voxel;
-    m[4 * i + 3] = (T[4 * i + 3] - o[i]) / g.voxel - 0.5;
+    for (int j = 0; j < 3; ++j) m[4 * i + j] = T[4 * i + j] * iv;
+    m[4 * i + 3] = (T[4 * i + 3] - o[i]) * iv - 0.5;
   }
 #pragma unroll
   for (int i = 0; i < 12; ++i) ok = ok && fabs(m[i]) < 1e30;
