@@ -160,9 +160,10 @@ __device__ __noinline__ void member_delta(const float* __restrict__ pst_row, dou
 // advantage set and Wsum the sum of the weights (|A| for the paper's plain mean).
 __device__ __noinline__ void apply_mean(const double* Q, const double* U, double Wsum, const double* P, int conv,
                                         double* Pn) {
-  const double qn = sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
-  const double qb[4] = {Q[0] / qn, Q[1] / qn, Q[2] / qn, Q[3] / qn};
-  const double ub[3] = {U[0] / Wsum, U[1] / Wsum, U[2] / Wsum};
+  const double iq = 1.0 / sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]);
+  const double iw = 1.0 / Wsum;
+  const double qb[4] = {Q[0] * iq, Q[1] * iq, Q[2] * iq, Q[3] * iq};
+  const double ub[3] = {U[0] * iw, U[1] * iw, U[2] * iw};
   double Rb[9], PP[12], out[12];
   quat_to_R(qb, Rb);
   for (int i = 0; i < 12; ++i) PP[i] = P[i];
@@ -171,14 +172,29 @@ __device__ __noinline__ void apply_mean(const double* Q, const double* U, double
 }
 
 // 256-thread fixed-shape tree over red[kUpdW][256] (result in red[c][0]); all threads must call.
+// Level s adds element t + s into element t (t < s), s = 128 ... 1: the levels >= 32 in shared
+// memory, the last five in warp 0 by shfl_down (the same pairs, so the same sums bit for bit).
 __device__ __forceinline__ void treeW(double (*red)[256], int tid) {
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
+  for (int s = 128; s >= 32; s >>= 1) {
     if (tid < s)
 #pragma unroll
       for (int c = 0; c < kUpdW; ++c) red[c][tid] += red[c][tid + s];
     __syncthreads();
   }
+  if (tid < 32) {
+    double v[kUpdW];
+#pragma unroll
+    for (int c = 0; c < kUpdW; ++c) v[c] = red[c][tid];
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1)
+#pragma unroll
+      for (int c = 0; c < kUpdW; ++c) v[c] += __shfl_down_sync(0xffffffffu, v[c], s);
+    if (tid == 0)
+#pragma unroll
+      for (int c = 0; c < kUpdW; ++c) red[c][0] = v[c];
+  }
+  __syncthreads();
 }
 
 // a7 contribution of particle k (E_k from its record) to one 256-particle update block:
