@@ -14,6 +14,8 @@ from tests.fixtures import f_track_inputs, golden
 from tests.parity import (assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
                           close_E)
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
@@ -224,6 +226,39 @@ def test_track_single_particle_and_empty_cloud(pft):
     np.testing.assert_array_equal(e["T"], c["T_init"])
     assert np.all(e["E"] == 1.0) and np.all(e["n"] == 0)
     assert all(int(f) & 4 for f in e["trace"][:, 19])
+    vol.close()
+
+
+@pytest.mark.parametrize("persistent", [True, False])
+def test_track_fresh_volume_is_lost(pft, persistent):
+    """Degenerate map: a reset volume (V = 1, W = 0) has no in-band cell, so every E_k = E_c = 1
+    (reading L6), no particle improves on the baseline (strict <, L12), the pose never moves and
+    the search size never shrinks (s-law factor 1 at E = 1): trace flags 'A empty' and 'lost' on
+    every iteration, equal to the oracle -- on both tracker paths (K = 61, ragged)."""
+    import subprocess
+    import sys
+    c = config_tiny(seed=2)
+    pst = make_pst(2, 61)
+    p = TrackParams(iters=3, stride=1)
+    vol = gpu_volume(pft, c["desc"])
+    if persistent:
+        r = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, p)
+    else:
+        env = dict(os.environ, PFT_TRACK_PERSISTENT="0")
+        code = ("import sys; sys.path.insert(0, %r); import numpy as np, torch, tests.test_gpu_parity as t; "
+                "import paper_2509_24236_b200 as pft; from synth.configs import config_tiny, make_pst, TrackParams; "
+                "c = config_tiny(seed=2); v = t.gpu_volume(pft, c['desc']); "
+                "r = t.run_track(pft, v, c['depth'], c['intr'], c['T_init'], make_pst(2, 61), TrackParams(iters=3, stride=1)); "
+                "np.savez(sys.argv[1], **{k: r[k] for k in ('T', 'E', 'n', 'trace')})") % ROOT
+        out = os.path.join(os.environ.get("TMPDIR", "/tmp"), "pft_fresh_ml.npz")
+        subprocess.check_call([sys.executable, "-c", code, out], env=env)
+        r = dict(np.load(out))
+    o = oracle.OracleVolume(c["desc"]).track(c["depth"], c["intr"], c["T_init"], pst, p)
+    assert_trace_parity(r["trace"], o["trace"], "fresh volume")
+    np.testing.assert_array_equal(r["T"], c["T_init"])
+    assert np.all(r["E"] == 1.0) and np.all(r["n"] == 0)
+    assert all((int(f) & 3) == 3 for f in r["trace"][:, 19])
+    assert np.all(r["trace"][:, 17] == p.omega0_deg) and np.all(r["trace"][:, 18] == p.v0_cm)
     vol.close()
 
 
