@@ -288,6 +288,19 @@ def run_ours(args):
         tj = json.load(open(tf))
         traffic = tj.get("dram_bytes_per_eval", 0) * evals_per_launch
 
+    # gather-replay ceiling (tools/gather_replay.py on the bench map): the evaluation's exact mask +
+    # record address stream replayed without arithmetic, next to the tracker on the same frame
+    gather_view = None
+    gr = os.path.join(ROOT, "profiles", "r01_gather_replay.jsonl")
+    if os.path.exists(gr):
+        rows = [json.loads(x) for x in open(gr) if x.strip()]
+        ref = [x for x in rows if x.get("init_noise_deg_cm") == 5.0 and x.get("frame") == 12] or rows
+        x = ref[0]
+        gather_view = {"replay_evals_per_s": x["replay_evals_per_s"], "track_evals_per_s": x["track_evals_per_s"],
+                       "frac": x["track_evals_per_s"] / x["replay_evals_per_s"], "inband_frac": x["inband_frac"],
+                       "source": "profiles/r01_gather_replay.jsonl (frame %d, +-%g deg/cm init)" % (
+                           x["frame"], x["init_noise_deg_cm"])}
+
     # ---- particle sweep (BASELINE config 4 sizes) on the same 512^3 map, one frame, 10 iterations
     sweep = {}
     if world == 1:
@@ -398,6 +411,7 @@ def run_ours(args):
                      "basis": f"{OPS_PER_EVAL} algorithmic ops/eval x {evals_per_launch:.0f} evals/launch / event time; "
                               f"peak = {n_sm} SMs x {LANES_PER_SM} lanes x {sm_mhz:.0f} MHz issue slots (DESIGN.md §7)",
                      "evals_per_s_kernel": evals_per_launch / avg_launch_s,
+                     "gather_view": gather_view,
                      "hbm_view": {"logical_gather_gbs": gather_gbs, "peak_gbs": hbm_peak, "frac": gather_gbs / hbm_peak,
                                   "note": f"{BYTES_PER_EVAL} B corner gather/eval, served from L2/L1 (DRAM traffic "
                                           "is 'traffic'); not the binding resource"}},

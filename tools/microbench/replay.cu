@@ -1,0 +1,71 @@
+// Gather-replay ceiling (SURVEY.md §8(d-3) roofline denominator (4)): replays the evaluation's
+// exact address stream -- per (particle, point) the cell's in-band mask word and then its 32-byte
+// record (record 0 when out of band), in the tracker's work-item order (4 tiles x 16 particles per
+// warp item from one dynamic queue, 4 points per lane batched) -- with no transform and no lerp.
+// The packed index stream (bit 31 in-band, bits 0..30 the record index) is precomputed on the host
+// by tools/gather_replay.py and streamed with evict-first loads (157 MB per iteration at config Q,
+// which makes the ceiling slightly pessimistic).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Xcompiler -fPIC -shared -o libreplay.so replay.cu
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace {
+__device__ __forceinline__ void ld32(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+__global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ idx, int K, int npad,
+                                                   const float* __restrict__ rec, const unsigned* __restrict__ mask,
+                                                   unsigned* __restrict__ queue, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int ngroups = npad / 128, nch = (K + 15) / 16;
+  const int nitems = ngroups * nch;
+  float acc = 0.f;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(queue, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nitems) break;
+    const int group = item / nch, chunk = item - group * nch;
+    const int k0 = chunk * 16, k1 = min(K, k0 + 16);
+    for (int k = k0; k < k1; ++k) {
+      uint32_t w[4], mw[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) w[p] = __ldcs(idx + (size_t)k * npad + (group * 4 + p) * 32 + lane);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) mw[p] = __ldg(mask + ((w[p] & 0x7fffffffu) >> 5));
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const uint32_t o = w[p] & 0x7fffffffu;
+        const uint32_t inb = (w[p] >> 31) & (mw[p] >> (o & 31u));  // the mask is all ones: inb, with the dependency
+        float v[8];
+        ld32(rec + (size_t)(o * inb) * 8, v);
+        acc += inb ? fabsf(v[0] + v[7]) : 0.f;
+      }
+    }
+  }
+  if (acc == 1234.5f) out[blockIdx.x] = acc;
+}
+}  // namespace
+
+extern "C" int replay_run(const uint32_t* idx, int K, int npad, const float* rec, const unsigned* mask, int reps,
+                          unsigned* queue, float* out, float* ms_out) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaMemset(queue, 0, 4);
+    cudaEventRecord(e0);
+    k_replay<<<296, 256>>>(idx, K, npad, rec, mask, queue, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;  // the first run is a warm-up
+  }
+  *ms_out = best;
+  return (int)cudaGetLastError();
+}
