@@ -221,6 +221,12 @@ class Volume:
         self._ws = {}
         return True
 
+    def comm_detach_p2p(self):
+        """Undo comm_init_p2p on this rank (single-rank again)."""
+        check(lib().pft_comm_p2p_detach(self.handle))
+        self.nranks, self.rank = 1, 0
+        self._ws = {}
+
     def close(self):
         if getattr(self, "handle", None):
             lib().pft_volume_destroy(self.handle)

@@ -199,3 +199,41 @@ def test_p2p_init_consensus_falls_back_together():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == {0: (False, 1), 1: (False, 1)}
+
+
+def _p2p_attach_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2509_24236_b200 as pft
+    from synth.configs import config_tiny
+    torch.cuda.set_device(0)
+    c = config_tiny(seed=1)
+    vol = pft.Volume(c["desc"], torch.device("cuda", 0))
+    ok = vol.comm_init_p2p(4096)  # real CUDA IPC between two processes (same device here)
+    state = (ok, vol.nranks, vol.rank)
+    if ok:
+        vol.comm_detach_p2p()
+        state = state + (vol.nranks,)
+    vol.close()
+    q.put((rank, state))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_p2p_ipc_attach_two_processes():
+    """F2 plumbing on real CUDA IPC: two processes (ranks) each allocate an exchange buffer, trade
+    IPC handles over torch.distributed, open each other's buffer and agree; then detach.  Only the
+    mapping is exercised -- no tracker kernels, so nothing waits on a peer (one GPU here)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_attach_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: (True, 2, 0, 1), 1: (True, 2, 1, 1)}, res
