@@ -42,12 +42,19 @@ def assert_pose_close(Ta, Tb, what=""):
 
 
 def assert_trace_parity(tr_gpu, tr_ora, what=""):
-    """Per-iteration: |A| exact, E_base / E(P) 1e-5 rel, s 1e-6 rel, P 1e-4, flags exact."""
+    """Per-iteration: |A| exact, E_base / E(P) 1e-5 rel, s 1e-6 rel, P 1e-4, flags exact; the
+    24-double rows' n_c, N, K_i and point-set code exact.  Rows after a stop rule fired are
+    "not run" (flag bit 5, include/pft.h): all zeros except the flag, on both sides."""
     tr_gpu = np.asarray(tr_gpu)
     for i in range(tr_ora.shape[0]):
         g, o = tr_gpu[i], tr_ora[i]
         w = f"{what} iter {i + 1}"
+        if int(o[19]) & 32:
+            assert np.array_equal(g, o), f"{w}: not-run row gpu={g} oracle={o}"
+            continue
         assert g[1] == o[1], f"{w}: |A| gpu={g[1]} oracle={o[1]}"
+        if len(o) > 20:
+            assert np.array_equal(g[20:24], o[20:24]), f"{w}: n_c/N/K_i/code gpu={g[20:24]} oracle={o[20:24]}"
         assert close_E(g[0], o[0]) and close_E(g[16], o[16]), f"{w}: E gpu={g[[0, 16]]} oracle={o[[0, 16]]}"
         for j in (2, 3, 17, 18):
             assert abs(g[j] - o[j]) <= 1e-6 * abs(o[j]) + 1e-12, f"{w}: s[{j}] gpu={g[j]} oracle={o[j]}"

@@ -135,3 +135,44 @@ def test_sweep_W_k4096_fused_exchange_G8(sweep):
     for k in ("T", "E", "n", "trace"):
         assert np.array_equal(a[k], b[k].cpu().numpy()), k
     v8.close()
+
+
+@pytest.mark.parametrize("variant", ["topk", "weighted_guard"])
+def test_sweep_W_k4096_update_variants(sweep, variant):
+    """NEXT row F3 at full size: config W, K = 4096, 10 iterations, with the top-32 mean or the
+    weighted mean + acceptance guard + stall stop -- the whole trace and the last iteration's
+    per-particle E_k / n_k against the oracle."""
+    import dataclasses
+    c, vol, ov = sweep
+    pst = c["pst"][:4096].copy()
+    extra = dict(update_rule=2, topk=32) if variant == "topk" else dict(update_rule=1, guard=1, stall_limit=3)
+    params = dataclasses.replace(TrackParams(iters=10, stride=4), **extra)
+    r = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), T(pst), params)
+    torch.cuda.synchronize()
+    o = ov.track(c["depth"], c["intr"], c["T_init"], pst, params)
+    assert_trace_parity(r["trace"].cpu().numpy(), o["trace"], f"W {variant}")
+    assert_last_iter_counts(r["n"].cpu().numpy(), r["E"].cpu().numpy(), o, ov, c["depth"], c["intr"], pst, params,
+                            c["T_init"], f"W {variant}")
+    assert_pose_close(r["T"].cpu().numpy(), o["T"])
+
+
+def test_sweep_W_paper_schedule(sweep):
+    """NEXT row F1 at full size: the paper's schedule on config W -- K cycling
+    10240 / 3072 / 1024 with 2-D strides (8,4) / (4,4) / (4,2), up to 20 iterations with the
+    min-search stop -- every trace row (incl. K_i, the stride code, n_c, the stop iteration) and
+    the last iteration's counts against the oracle."""
+    import dataclasses
+    from synth.configs import PAPER_SCHEDULE
+    c, vol, ov = sweep
+    pst = c["pst"][:10240].copy()
+    params = dataclasses.replace(TrackParams(iters=20, stride=4), **PAPER_SCHEDULE)
+    r = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), T(pst), params)
+    torch.cuda.synchronize()
+    o = ov.track(c["depth"], c["intr"], c["T_init"], pst, params)
+    tr = r["trace"].cpu().numpy()
+    assert_trace_parity(tr, o["trace"], "W paper schedule")
+    n, E = r["n"].cpu().numpy(), r["E"].cpu().numpy()
+    mism = int((n != o["n"]).sum())
+    assert mism == 0, f"{mism} last-iteration count mismatches"
+    assert close_E(E, o["E"]).all()
+    assert_pose_close(r["T"].cpu().numpy(), o["T"])
