@@ -493,6 +493,9 @@ def _fused_cases():
                 dataclasses.replace(TrackParams(iters=7, stride=1, guard=1, update_rule=1), **SCHED_TINY)))
     c = config_tiny(seed=1)
     out.append(("tiny_stop", c, c["pst"], TrackParams(iters=8, stride=2, min_search_deg=4.0, min_search_cm=1e9)))
+    c = dict(with_desc(config_tiny(seed=3), storage="f16"))
+    c["V"], c["W"] = c["V"].astype(np.float16), c["W"].astype(np.float16)
+    out.append(("tiny16_world", c, c["pst"], TrackParams(iters=4, stride=1, delta_conv=1)))
     return out
 
 
