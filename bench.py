@@ -495,7 +495,26 @@ def cpu_baseline(args, seq, map_depth, steps, budget_s=10.0):
         nf += 1
         if dt >= budget_s:
             break
+    # effective parallelism: the same one-frame track on 1 thread vs all cores,
+    # on a small particle subset
+    s0 = steps[0]
+    sub = seq.pst[:128].copy()
+    t1 = time.perf_counter()
+    ov.track(s0["depth"], seq.intr, s0["T_init"], sub, seq.params, nthreads=1)
+    t1 = time.perf_counter() - t1
+    tn = time.perf_counter()
+    ov.track(s0["depth"], seq.intr, s0["T_init"], sub, seq.params, nthreads=cores())
+    tn = time.perf_counter() - tn
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"value": ev / dt, "unit": "evals/s", "cores": cores(), "kind": "oracle",
+            "cpu_model": model, "effective_parallelism": t1 / tn,
             "sample": f"{nf} frame(s) of full RO tracking ({len(seq.pst)} particles x {seq.params.iters} iterations "
                       f"x {r['N']} points) on a 512^3 fp32 map fused by the oracle from {len(map_depth)} frames; "
                       f"{dt:.1f} s"}
