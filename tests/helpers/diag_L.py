@@ -1,6 +1,6 @@
 """Diagnostic: config L lock-step; for any n_k mismatch report the oracle's decision margin."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle, paper_2509_24236_b200 as pft
 from synth.configs import Sequence
