@@ -176,3 +176,22 @@ def test_sweep_W_paper_schedule(sweep):
     assert mism == 0, f"{mism} last-iteration count mismatches"
     assert close_E(E, o["E"]).all()
     assert_pose_close(r["T"].cpu().numpy(), o["T"])
+
+
+@pytest.mark.parametrize("variant", ["mean", "topk", "weighted_guard"])
+def test_sweep_W_k65536_two_iterations(sweep, variant):
+    """Config W at the largest K (65536: 256 update blocks, the top-k merge over 256 sorted
+    lists), 2 iterations of each update rule: both trace rows and all 65536 last-iteration E_k /
+    n_k against the oracle."""
+    import dataclasses
+    c, vol, ov = sweep
+    extra = {"mean": {}, "topk": dict(update_rule=2, topk=32),
+             "weighted_guard": dict(update_rule=1, guard=1)}[variant]
+    params = dataclasses.replace(TrackParams(iters=2, stride=4), **extra)
+    r = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), T(c["pst"]), params)
+    torch.cuda.synchronize()
+    o = ov.track(c["depth"], c["intr"], c["T_init"], c["pst"], params)
+    assert_trace_parity(r["trace"].cpu().numpy(), o["trace"], f"W K=65536 {variant}")
+    assert_last_iter_counts(r["n"].cpu().numpy(), r["E"].cpu().numpy(), o, ov, c["depth"], c["intr"], c["pst"],
+                            params, c["T_init"], f"W K=65536 {variant}")
+    assert_pose_close(r["T"].cpu().numpy(), o["T"])
