@@ -195,3 +195,22 @@ def test_sweep_W_k65536_two_iterations(sweep, variant):
     assert_last_iter_counts(r["n"].cpu().numpy(), r["E"].cpu().numpy(), o, ov, c["depth"], c["intr"], c["pst"],
                             params, c["T_init"], f"W K=65536 {variant}")
     assert_pose_close(r["T"].cpu().numpy(), o["T"])
+
+
+def test_sweep_W_k4096_virtual_shards_G4(sweep):
+    """The multi-launch sharded path (NCCL all-gather replaced by device copies, 4 virtual ranks)
+    at config W, K = 4096, 10 iterations: bit-identical to the 1-rank persistent run."""
+    import paper_2509_24236_b200 as pft
+    c, vol, ov = sweep
+    pst = T(c["pst"][:4096].copy())
+    params = TrackParams(iters=10, stride=4)
+    a = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
+    a = {k: a[k].cpu().numpy() for k in ("T", "E", "n", "trace")}
+    v4 = pft.Volume(c["desc"], dev())
+    v4.upload(c["V"], c["W"])
+    v4.comm_init_virtual(4)
+    b = v4.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
+    torch.cuda.synchronize()
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(a[k], b[k].cpu().numpy()), k
+    v4.close()
