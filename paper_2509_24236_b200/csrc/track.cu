@@ -1729,6 +1729,10 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   cudaError_t e = cudaSuccess;
   PFT_LAUNCH(PFT_PROF_TRACK, c.st,
              e = cudaLaunchCooperativeKernel((const void*)k_track_persistent<T>, dim3(grid), dim3(kThreads), args, 0, c.st));
+  if (e == cudaErrorCooperativeLaunchTooLarge && G == 1 && !emul) {
+    cudaGetLastError();  // not sticky: the SMs are partly taken (e.g. by another context)
+    return PFT_ERR_UNSUPPORTED;  // the caller falls back to the multi-launch tracker
+  }
   if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "persistent tracker launch: %s", cudaGetErrorString(e));
   return cuda_check("track (persistent)");
 }
@@ -1746,8 +1750,11 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
                             const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                             int32_t* n_out, double* trace) {
   const int G = c.vol->nranks, r = c.vol->rank;
-  if ((G == 1 || c.vol->virtual_fused || c.vol->p2p) && use_persistent() && prm->iters <= 1024)
-    return track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
+  if ((G == 1 || c.vol->virtual_fused || c.vol->p2p) && use_persistent() && prm->iters <= 1024) {
+    const pft_status s = track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
+    if (s != PFT_ERR_UNSUPPORTED) return s;
+    // the cooperative grid does not fit right now (G = 1): same results from the multi-launch path
+  }
   const int kloc = c.L.kloc;
   const int k_begin = r * kloc;
   PartRec* local = (PartRec*)(c.ws + c.L.acc_local_off);
