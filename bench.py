@@ -11,8 +11,10 @@ pose.  The TSDF is first built by integrating `--map-frames` frames of the traje
   python bench.py --impl reference [...]                   # the fp64 CPU oracle on a bounded sample
 
 Multi-GPU (torchrun, one rank per GPU): particles are sharded (K = 2048 * N in total, weak
-scaling), the volume is replicated, per-particle results are all-gathered over NCCL each
-iteration.  Timing: CUDA events around each step on the launching stream, L2 flushed (256 MiB
+scaling), the volume is replicated, and each iteration's per-particle records reach every rank
+through the F2 exchange inside the persistent tracker (P2P stores over NVLink; `--exchange nccl`
+for the ncclAllGather path).  Each frame is replayed as a CUDA graph (`--no-graph` for eager
+calls).  Timing: CUDA events around each step on the launching stream, L2 flushed (256 MiB
 write) between steps outside the events, max over ranks.
 """
 import argparse
