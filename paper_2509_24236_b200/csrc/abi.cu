@@ -223,7 +223,7 @@ pft_status pft_comm_init_virtual_fused(pft_volume* vol, int32_t nranks) {
   vol->virtual_ranks = nranks > 1 ? nranks : 0;
   vol->virtual_fused = nranks > 1 ? 1 : 0;
   vol->xws_last = nullptr;
-  vol->xws_total = 0;
+  vol->xws_total = vol->xws_region = vol->xws_xcnt = 0;
   return PFT_OK;
 }
 

@@ -78,7 +78,7 @@ struct pft_volume {
   int32_t xmax_particles;
   // one-GPU emulation: the exchange counters are zeroed when the workspace changes
   const char* xws_last;
-  size_t xws_total;
+  size_t xws_total, xws_region, xws_xcnt;  // workspace + layout the counters were zeroed for
 };
 
 namespace pft {

@@ -1712,11 +1712,15 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
     pa.o_xcnt = c.L.xcnt_rel;
     pa.xhalf = (size_t)c.L.kfull;  // emulation: one launch at a time, so a per-call stride is safe
     // the counters are monotone across calls (pft.h: F2 exchange); a new workspace starts them at 0
-    if (vol->xws_last != c.ws || vol->xws_total != c.L.total) {
+    // the counters' location depends on the layout (K, G), not only on the workspace pointer
+    if (vol->xws_last != c.ws || vol->xws_total != c.L.total || vol->xws_region != region ||
+        vol->xws_xcnt != c.L.xch_off + c.L.xcnt_rel) {
       for (int q = 0; q < G; ++q)
         cudaMemsetAsync(pa.xbuf[q] + pa.o_xcnt, 0, (kMaxFusedRanks + 1) * sizeof(unsigned long long), c.st);
       vol->xws_last = c.ws;
       vol->xws_total = c.L.total;
+      vol->xws_region = region;
+      vol->xws_xcnt = c.L.xch_off + c.L.xcnt_rel;
     }
   } else if (G > 1) {
     if (Kp > vol->xmax_particles)

@@ -536,3 +536,23 @@ def test_fused_exchange_one_launch(pft):
     run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"], c["params"])
     assert pft.launch_count() - n0 == 1
     vol.close()
+
+
+def test_fused_exchange_counters_follow_the_layout(pft):
+    """F2 emulation: consecutive calls on ONE workspace buffer with different K (so the exchange
+    counters move) -- each call still equals its 1-rank run (the counters are re-zeroed whenever
+    the layout changes, include/pft.h)."""
+    c = config_single(seed=1)
+    ref = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    vol.comm_init_virtual(3, fused=True)
+    big = torch.empty(1 << 28, dtype=torch.uint8, device=dev())
+    vol.workspace = lambda intr, K, params: big
+    for K in (1024, 1000, 1024, 517):
+        pst = make_pst(4, K)
+        a = run_track(pft, ref, c["depth"], c["intr"], c["T_init"], pst, c["params"])
+        b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, c["params"])
+        for k in ("T", "E", "n", "trace"):
+            assert np.array_equal(a[k], b[k]), (K, k)
+    ref.close()
+    vol.close()
