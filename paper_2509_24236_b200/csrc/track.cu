@@ -446,9 +446,10 @@ __device__ __forceinline__ void eval_points_f64(const T* __restrict__ V, const u
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const unsigned long long mw = __ldg(mask + (o[p] >> 6));
+    // exact stored corner values (brick order), not the record; loaded together with the mask
+    // word (one round trip), used only when the cell is in band
+    const uint32_t b = o[p];
     ok[p] = ok[p] && ((mw >> (o[p] & 63)) & 1ull);
-    // exact stored corner values (brick order), not the record
-    const uint32_t b = ok[p] ? o[p] : 0u;
     const uint32_t dx = ((b & 3u) == 3u) ? 64u - 3u : 1u;              // x + 1 crosses into the next brick?
     const uint32_t dy = (((b >> 2) & 3u) == 3u) ? g.sy - 12u : 4u;
     const uint32_t dz = (((b >> 4) & 3u) == 3u) ? g.sz - 48u : 16u;
