@@ -462,7 +462,7 @@ def run_ours(args):
                            "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),
                            "note": "paper-literal RO from GT (+) U+-5deg/+-5cm, per frame (SURVEY.md 8(c-5))"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
         res["cpu_baseline"] = cpu_baseline(args, seq, map_depth, [steps_in[i] for i in idx])
     if rank == 0:
         print(json.dumps(res), flush=True)
