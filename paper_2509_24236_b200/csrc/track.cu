@@ -943,7 +943,10 @@ __global__ void k_track_finalize(const TrackState* st, int K, double* E_out, int
 //      decisions); CTA 0 writes the trace.
 // Results are bit-identical to the multi-launch path (same helpers, integer sums, same trees).
 constexpr int kItemTiles = 4;     // 8x4 tiles per warp item (= PPT 4 points per lane)
-constexpr int kItemParticles = 16;
+#ifndef PFT_ITEM_PARTICLES
+#define PFT_ITEM_PARTICLES 16
+#endif
+constexpr int kItemParticles = PFT_ITEM_PARTICLES;
 
 struct PArgs {
   const void* R;
@@ -1071,8 +1074,8 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
   constexpr size_t kTopBytes = 256 * (sizeof(unsigned long long) + sizeof(int));
   constexpr size_t kPartBytes = (kThreads / 32) * kItemParticles * 33 * sizeof(unsigned long long);
-  static_assert(kRedBytes + kTopBytes <= kPartBytes, "union layout");
-  __shared__ __align__(16) unsigned char sUnion[kPartBytes];
+  constexpr size_t kUnionBytes = kPartBytes > kRedBytes + kTopBytes ? kPartBytes : kRedBytes + kTopBytes;
+  __shared__ __align__(16) unsigned char sUnion[kUnionBytes];
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12], sPprev[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
