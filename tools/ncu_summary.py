@@ -18,6 +18,7 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sector_hit_rate.pct",
         "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sectors.sum.per_second", "dram__bytes.sum.per_second",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
@@ -70,6 +71,12 @@ def report(path, evals=None):
                        f"shared wavefronts/eval {num('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum') / evals:.3f}; "
                        f"sectors/request {num('l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum') / max(1, num('l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum')):.2f}; "
                        f"warp instr/warp-eval {num("smsp__inst_executed.sum") / (evals / 32):.1f}")
+        if "lts__t_sectors.sum.per_second" in vals:
+            u = units[h.index("lts__t_sectors.sum.per_second")]
+            per = {"sector/ns": 1e9, "sector/us": 1e6, "sector/ms": 1e3, "sector/s": 1.0}.get(u, 1.0)
+            sec_s = float(vals["lts__t_sectors.sum.per_second"].replace(",", "")) * per
+            out.append(f"  achieved L2 throughput {sec_s * 32 / 1e9:.0f} GB/s (32-byte sectors; "
+                       f"{num('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f}% of the L2 peak)")
     return "\n".join(out)
 
 
