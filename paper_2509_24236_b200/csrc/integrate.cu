@@ -13,6 +13,10 @@
 // margins) compacts the 4^3 bricks that can contain an updated voxel; the fusion kernel then
 // sweeps only those bricks, 64 consecutive elements (one brick = 2 x 128 B lines per array
 // at fp32) per pair of warps, fully coalesced.  The full sweep is kept for verification.
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "pft_internal.cuh"
 
 namespace pft {
@@ -20,6 +24,7 @@ namespace pft {
 struct Intr {
   double fx, fy, cx, cy, unit;
   int W, H;
+  bool c_small;  // |cx|, |cy| < 2^19: pixel_of's guarded fast path applies
 };
 
 template <typename T> __device__ __forceinline__ double to_double(T x);
@@ -41,39 +46,78 @@ __device__ __forceinline__ double i2d(int i) {  // 0 <= i < 2^31
 // floor(x) in its low word.
 __device__ __forceinline__ int floor_lo(double x) { return __double2loint(__dadd_rd(x, 6755399441055744.0)); }
 
-// Returns true iff the stored value V changed (its cell records must then be refreshed).
+// Pixel index floor(u2) of u2 = RN(RN(RN(p / z) + c) + 1/2), the oracle's expression (p = RN(f x)),
+// given rz = RN(1/z) shared by both image axes.  Fast path: qa = RN(p rz) differs from RN(p/z) by
+// at most 1.5 ulp, so for |qa| < 2^19 and |c| < 2^19 the approximate u2a is within 2^-30 of u2
+// (two more roundings of values < 2^21, ulp 2^-32 each); whenever the fraction of u2a is at least
+// 2^-26 away from an integer, floor(u2a) = floor(u2) -- the same decision.  Otherwise (a guard-band
+// hit, ~1e-8 of the voxels, or a huge |qa|) the exact IEEE division decides.  Returns false when the
+// pixel is outside [0, n) (also for |u2| >= 2^30 and NaN).
+__device__ __forceinline__ bool pixel_of(double p, double z, double rz, double c, bool c_small, int n, int& pix) {
+  const double qa = __dmul_rn(p, rz);
+  if (c_small && fabs(qa) < 524288.0) {
+    const double u2a = __dadd_rn(__dadd_rn(qa, c), 0.5);
+    const double t = __dadd_rd(u2a, 6755399441055744.0);         // floor(u2a) in the low word
+    const double fr = __dsub_rn(u2a, __dsub_rn(t, 6755399441055744.0));  // exact: |u2a| < 2^20
+    if (fr >= 1.4901161193847656e-08 && fr <= 1.0 - 1.4901161193847656e-08) {
+      pix = __double2loint(t);
+      return (unsigned)pix < (unsigned)n;
+    }
+  }
+  const double u2 = __dadd_rn(__dadd_rn(__ddiv_rn(p, z), c), 0.5);
+  if (!(fabs(u2) < 1073741824.0)) return false;
+  pix = floor_lo(u2);
+  return (unsigned)pix < (unsigned)n;
+}
+
+// Per-frame axis tables (fusion step 1, computed by k_frame_prep).  The oracle's camera coordinates are
+//   x = RN(RN(RN(R00 d0) + RN(R10 d1)) + RN(R20 d2)),  d_a = RN(g_a - t_a),  g_a = RN(o_a + RN(s RN(i_a + 1/2)))
+// (T = [R|t] row-major, so x pairs with T[0], T[4], T[8]; y with T[1], T[5], T[9]; z with T[2], T[6],
+// T[10]).  Each product depends on one axis index only, so the 9 rounded products are tabulated once
+// per frame per axis index, {RN(T[4a] d_a), RN(T[4a+1] d_a), RN(T[4a+2] d_a)} for axis a, and a voxel
+// needs 3 table loads and 6 additions in the oracle's order -- the same bits.
+__device__ __forceinline__ double4 ld_axis(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// Vs, Ws: the voxel's stored value and weight, loaded by the caller ahead of the dependent chain
+// (their addresses depend on nothing computed here).  Returns true iff the stored value V changed
+// (its cell records must then be refreshed).  Stored bits equal the oracle's: every value that reaches storage (z, sdf, v_new, V', W') is
+// computed with the oracle's exact operations (x, y, z from the axis tables in its order); the
+// projection only decides a pixel (pixel_of's guarded reciprocal), and two divisions are skipped
+// where their correctly rounded result is known exactly: v_new = 1 when sdf >= tau (then
+// sdf/tau >= 1, rounded >= 1, clamped to 1), and V' = 1 when V = 1 and v_new = 1 (numerator
+// RN(1*W + 1) and denominator RN(W + 1) are the same finite a >= 1, and a/a = 1) -- the free space
+// in front of the surface, most updated voxels.
 template <typename T>
 __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
-                                           const double* T_, int i, int j, int k, T* __restrict__ V,
-                                           T* __restrict__ W, uint32_t o) {
-  const double gw0 = __dadd_rn(g.ox, __dmul_rn(g.voxel, __dadd_rn(i2d(i), 0.5)));
-  const double gw1 = __dadd_rn(g.oy, __dmul_rn(g.voxel, __dadd_rn(i2d(j), 0.5)));
-  const double gw2 = __dadd_rn(g.oz, __dmul_rn(g.voxel, __dadd_rn(i2d(k), 0.5)));
-  const double d0 = __dsub_rn(gw0, T_[3]), d1 = __dsub_rn(gw1, T_[7]), d2 = __dsub_rn(gw2, T_[11]);
-  const double z = __dadd_rn(__dadd_rn(__dmul_rn(T_[2], d0), __dmul_rn(T_[6], d1)), __dmul_rn(T_[10], d2));
+                                           const double4& A, const double4& B, const double4& C, T Vs, T Ws,
+                                           T* __restrict__ V, T* __restrict__ W, uint32_t o) {
+  const double z = __dadd_rn(__dadd_rn(A.z, B.z), C.z);
   if (!(z > 0.0)) return false;
-  const double x = __dadd_rn(__dadd_rn(__dmul_rn(T_[0], d0), __dmul_rn(T_[4], d1)), __dmul_rn(T_[8], d2));
-  const double y = __dadd_rn(__dadd_rn(__dmul_rn(T_[1], d0), __dmul_rn(T_[5], d1)), __dmul_rn(T_[9], d2));
-  // pixel = floor(u + 1/2): out of [0, W) also for |u + 1/2| >= 2^30 and NaN
-  const double u2 = __dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(K.fx, x), z), K.cx), 0.5);
-  if (!(fabs(u2) < 1073741824.0)) return false;
-  const int ui = floor_lo(u2);
-  if ((unsigned)ui >= (unsigned)K.W) return false;
-  const double v2 = __dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(K.fy, y), z), K.cy), 0.5);
-  if (!(fabs(v2) < 1073741824.0)) return false;
-  const int vi = floor_lo(v2);
-  if ((unsigned)vi >= (unsigned)K.H) return false;
+  const double x = __dadd_rn(__dadd_rn(A.x, B.x), C.x);
+  const double y = __dadd_rn(__dadd_rn(A.y, B.y), C.y);
+  const double rz = __drcp_rn(z);
+  int ui, vi;
+  if (!pixel_of(__dmul_rn(K.fx, x), z, rz, K.cx, K.c_small, K.W, ui)) return false;
+  if (!pixel_of(__dmul_rn(K.fy, y), z, rz, K.cy, K.c_small, K.H, vi)) return false;
   const uint16_t raw = __ldg(depth + (size_t)vi * K.W + (size_t)ui);
   const double d = __dmul_rn(i2d((int)raw), K.unit);
   if (raw == 0 || !(d < g.max_depth)) return false;
   const double sdf = __dsub_rn(d, z);
   if (!(sdf > -g.trunc)) return false;
-  double vnew = __ddiv_rn(sdf, g.trunc);
-  if (vnew > 1.0) vnew = 1.0;
-  const T Vs = V[o];
-  const double Vo = to_double<T>(Vs), Wo = to_double<T>(W[o]);
+  double vnew = 1.0;
+  if (!(sdf >= g.trunc)) {
+    vnew = __ddiv_rn(sdf, g.trunc);
+    if (vnew > 1.0) vnew = 1.0;
+  }
+  const double Vo = to_double<T>(Vs), Wo = to_double<T>(Ws);
   const double Wp = __dadd_rn(Wo, 1.0);
-  const double Vn = __ddiv_rn(__dadd_rn(__dmul_rn(Vo, Wo), vnew), Wp);
+  const double Vn = (vnew == 1.0 && Vo == 1.0 && Wo >= 0.0 && Wo <= 1e300)
+                        ? 1.0
+                        : __ddiv_rn(__dadd_rn(__dmul_rn(Vo, Wo), vnew), Wp);
   const double Wn = Wp > g.max_weight ? g.max_weight : Wp;
   const T Vnew = store_rn<T>(Vn);
   V[o] = Vnew;
@@ -84,11 +128,9 @@ __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const u
 // Full sweep: one thread per brick element (the verification path).
 template <typename T>
 __global__ __launch_bounds__(256) void k_integrate_sweep(Geom g, Intr K, const uint16_t* __restrict__ depth,
-                                                         const double* __restrict__ Tdev, T* __restrict__ V,
+                                                         const double4* __restrict__ tab, T* __restrict__ V,
                                                          T* __restrict__ W, size_t nelem) {
-  __shared__ double sT[12];
-  if (threadIdx.x < 12) sT[threadIdx.x] = Tdev[threadIdx.x];
-  __syncthreads();
+  const int n0 = 4 * g.nbx, n1 = 4 * g.nby;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < nelem; e += (size_t)gridDim.x * blockDim.x) {
     const uint32_t b = (uint32_t)(e >> 6), w = (uint32_t)(e & 63);
     const int bx = (int)(b % (uint32_t)g.nbx);
@@ -96,104 +138,177 @@ __global__ __launch_bounds__(256) void k_integrate_sweep(Geom g, Intr K, const u
     const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
     const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
     if (i >= g.nx || j >= g.ny || k >= g.nz) continue;
-    fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, (uint32_t)e);
+    fuse_voxel<T>(g, K, depth, ld_axis(tab + i), ld_axis(tab + n0 + j), ld_axis(tab + n0 + n1 + k), V[e], W[e], V, W,
+                  (uint32_t)e);
   }
 }
 
 // ---- culling ---------------------------------------------------------------------------------
-constexpr int kTile = 8;  // depth tiles of 8x8 pixels
+// Depth pyramid: level l holds, per tile of (8 << l) x (8 << l) pixels, {max valid raw depth,
+// ~min over the tile's pixels of (valid ? raw : 0)} (validity is the exact fp64 test of O1,
+// raw > 0 and raw * unit < max_depth; the minimum is stored complemented so that both halves are
+// maxima with identity 0).  A box's footprint is bounded by at most 4 x 4 tiles of the finest
+// level whose tiles it spans at most 4 of per axis: 16 independent loads in one round trip.
+constexpr int kTile = 8;
+constexpr int kLevels = 6;  // tiles of 8, 16, 32, 64, 128, 256 pixels
+struct Pyr {
+  int W, H;   // image size; level l has nx(l) x ny(l) tiles starting at element off(l)
+  int total;  // elements (uint2) of all levels
+  __host__ __device__ __forceinline__ int nx(int l) const { return (W + (kTile << l) - 1) >> (3 + l); }
+  __host__ __device__ __forceinline__ int ny(int l) const { return (H + (kTile << l) - 1) >> (3 + l); }
+  __host__ __device__ __forceinline__ int off(int l) const {
+    int o = 0;
+    for (int q = 0; q < l; ++q) o += nx(q) * ny(q);
+    return o;
+  }
+};
 
-// Per tile: the maximum valid raw depth (0 if the tile has no valid pixel).  Validity is the
-// exact fp64 test of O1 (raw > 0 and raw*unit < max_depth).
-__global__ void k_depth_tiles(Intr K, double max_depth, const uint16_t* __restrict__ depth, uint32_t* __restrict__ tiles,
-                              int ntx, int nty) {
-  const int t = blockIdx.x * blockDim.y + threadIdx.y;  // one warp per tile
-  if (t >= ntx * nty) return;
-  const int tx = t % ntx, ty = t / ntx;
-  uint32_t m = 0;
-  for (int p = threadIdx.x; p < kTile * kTile; p += 32) {
-    const int u = tx * kTile + (p & 7), v = ty * kTile + (p >> 3);
-    if (u < K.W && v < K.H) {
-      const uint16_t raw = depth[(size_t)v * K.W + u];
-      if (raw != 0 && __dmul_rn((double)raw, K.unit) < max_depth) m = max(m, (uint32_t)raw);
+static Pyr make_pyr(int W, int H) {
+  Pyr p{W, H, 0};
+  p.total = p.off(kLevels);
+  return p;
+}
+
+__device__ __forceinline__ uint2 tmax(uint2 a, uint2 b) { return make_uint2(max(a.x, b.x), max(a.y, b.y)); }
+
+// Frame preparation (one launch): CTAs [0, nreg) build the depth pyramid, one per 64 x 64-pixel
+// region (a level-3 tile): its 64 level-0 tiles by warps, levels 1-3 from shared memory, levels 4-5
+// by atomicMax (zeroed beforehand); the remaining CTAs compute the axis tables.
+__global__ __launch_bounds__(256) void k_frame_prep(Intr K, double max_depth, const uint16_t* __restrict__ depth,
+                                                    uint2* __restrict__ tiles, Pyr P, int nreg, Geom g,
+                                                    const double* __restrict__ Tdev, double4* __restrict__ tab) {
+  if ((int)blockIdx.x >= nreg) {
+    const int n0 = 4 * g.nbx, n1 = 4 * g.nby, n2 = 4 * g.nbz;
+    const int e = ((int)blockIdx.x - nreg) * 256 + threadIdx.x;
+    if (e < n0 + n1 + n2) {
+      const int a = e < n0 ? 0 : (e < n0 + n1 ? 1 : 2);
+      const int i = e - (a == 0 ? 0 : (a == 1 ? n0 : n0 + n1));
+      const double o = a == 0 ? g.ox : (a == 1 ? g.oy : g.oz);
+      const double gw = __dadd_rn(o, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
+      const double d = __dsub_rn(gw, Tdev[3 + 4 * a]);
+      tab[e] = make_double4(__dmul_rn(Tdev[4 * a], d), __dmul_rn(Tdev[4 * a + 1], d), __dmul_rn(Tdev[4 * a + 2], d),
+                            0.0);
+    }
+    return;
+  }
+  __shared__ uint2 s0[64], s1[16], s2[4];
+  const int nx3 = P.nx(3);
+  const int rx = (int)blockIdx.x % nx3, ry = (int)blockIdx.x / nx3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nx0 = P.nx(0), ny0 = P.ny(0);
+  int raw[16];  // all 16 pixel loads of this lane in flight together; -1: outside the image
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int ti = warp * 8 + (q >> 1), p = lane + 32 * (q & 1);
+    const int u = (rx * 8 + (ti & 7)) * kTile + (p & 7), v = (ry * 8 + (ti >> 3)) * kTile + (p >> 3);
+    raw[q] = (u < K.W && v < K.H) ? (int)__ldg(depth + (size_t)v * K.W + u) : -1;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int ti = warp * 8 + q;
+    const int tx = rx * 8 + (ti & 7), ty = ry * 8 + (ti >> 3);
+    uint2 m = make_uint2(0u, 0u);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = raw[2 * q + h];
+      if (r >= 0) {
+        const bool valid = r != 0 && __dmul_rn((double)r, K.unit) < max_depth;
+        m = tmax(m, make_uint2(valid ? (uint32_t)r : 0u, ~(valid ? (uint32_t)r : 0u)));
+      }
+    }
+    for (int sft = 16; sft > 0; sft >>= 1)
+      m = tmax(m, make_uint2(__shfl_xor_sync(0xffffffffu, m.x, sft), __shfl_xor_sync(0xffffffffu, m.y, sft)));
+    if (lane == 0) {
+      s0[ti] = m;
+      if (tx < nx0 && ty < ny0) tiles[ty * nx0 + tx] = m;
     }
   }
-  for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
-  if (threadIdx.x == 0) {
-    tiles[t] = m;
-    if (m) atomicMax(tiles + ntx * nty + (ty >> 3) * ((ntx + 7) >> 3) + (tx >> 3), m);  // coarse 64x64-px level
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < 16) {
+    const int a = t & 3, b = t >> 2;
+    const uint2 m = tmax(tmax(s0[16 * b + 2 * a], s0[16 * b + 2 * a + 1]), tmax(s0[16 * b + 8 + 2 * a], s0[16 * b + 9 + 2 * a]));
+    s1[t] = m;
+    const int X = rx * 4 + a, Y = ry * 4 + b;
+    if (X < P.nx(1) && Y < P.ny(1)) tiles[P.off(1) + Y * P.nx(1) + X] = m;
+  }
+  __syncthreads();
+  if (t < 4) {
+    const int a = t & 1, b = t >> 1;
+    const uint2 m = tmax(tmax(s1[8 * b + 2 * a], s1[8 * b + 2 * a + 1]), tmax(s1[8 * b + 4 + 2 * a], s1[8 * b + 5 + 2 * a]));
+    s2[t] = m;
+    const int X = rx * 2 + a, Y = ry * 2 + b;
+    if (X < P.nx(2) && Y < P.ny(2)) tiles[P.off(2) + Y * P.nx(2) + X] = m;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const uint2 m = tmax(tmax(s2[0], s2[1]), tmax(s2[2], s2[3]));
+    tiles[P.off(3) + ry * nx3 + rx] = m;
+    uint2* t4 = tiles + P.off(4) + (ry >> 1) * P.nx(4) + (rx >> 1);
+    uint2* t5 = tiles + P.off(5) + (ry >> 2) * P.nx(5) + (rx >> 2);
+    if (m.x) { atomicMax(&t4->x, m.x); atomicMax(&t5->x, m.x); }
+    if (m.y) { atomicMax(&t4->y, m.y); atomicMax(&t5->y, m.y); }
   }
 }
 
-// Conservative visibility test of a box of voxel centres given by its centre (world, fp64) and
-// bounding-sphere radius: false only when no voxel centre inside can pass the voxel-level tests
-// (all z_c <= 0, projection misses the image, or every pixel it can project to is invalid or has
-// d + tau <= z_c).  fp32 with margins (1 mm, 2 px) far above fp32 rounding at room scale.  Boxes
-// straddling the camera plane, or covering more than max_tiles depth tiles, are kept.
-struct Footprint {
-  int verdict;  // 0 reject, 1 keep, 2 decided by the max depth over tiles [t0x,t1x] x [t0y,t1y] of lvl
-  const uint32_t* lvl;
-  int stride, t0x, t1x, t0y, t1y;
-  float zn;
-};
+// Conservative classification of a box of voxel centres given by its centre (world, fp64) and
+// bounding-sphere radius, in fp32 with margins (1 mm, 2 px) far above fp32 rounding at room scale:
+//   CULL  no voxel centre inside can pass the voxel-level tests (all z_c <= 0, the projection misses
+//         the image, or every pixel it can project to is invalid or has d + tau <= z_c);
+//   FREE  every voxel centre inside projects into the image onto a valid pixel with d - z_c >= tau:
+//         each is updated with v_new = 1, whatever its exact pixel (the "free space" class);
+//   KEEP  otherwise (incl. boxes straddling the camera plane or wider than 4 coarsest tiles).
+enum { kCull = 0, kKeep = 1, kFree = 2 };
 
-__device__ __forceinline__ Footprint box_footprint(const Intr& K, const double* __restrict__ Tdev,
-                                                   const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
-                                                   double czw, float rad, int max_tiles) {
-  Footprint f;
-  f.verdict = 0;
+__device__ __forceinline__ int box_class(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
+                                         const uint2* __restrict__ tiles, const Pyr& P, double cxw, double cyw,
+                                         double czw, float rad, int lane16) {
   const float cwx = (float)(cxw - Tdev[3]), cwy = (float)(cyw - Tdev[7]), cwz = (float)(czw - Tdev[11]);
   const float x = (float)Tdev[0] * cwx + (float)Tdev[4] * cwy + (float)Tdev[8] * cwz;
   const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
   const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
-  if (!(z + rad > 0.f)) return f;
-  f.verdict = 1;
-  if (z - rad <= 1e-3f) return f;  // straddles the camera plane: no projection bound
+  if (!(z + rad > 0.f)) return kCull;
+  if (z - rad <= 1e-3f) return kKeep;  // straddles the camera plane: no projection bound
   const float zn = z - rad, zf = z + rad;
   const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
-  const float u0 = fx * fminf((x - rad) / zn, (x - rad) / zf) + cx - 2.f;
-  const float u1 = fx * fmaxf((x + rad) / zn, (x + rad) / zf) + cx + 2.f;
-  const float v0 = fy * fminf((y - rad) / zn, (y - rad) / zf) + cy - 2.f;
-  const float v1 = fy * fmaxf((y + rad) / zn, (y + rad) / zf) + cy + 2.f;
-  f.verdict = 0;
-  if (!(u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H)) return f;
+  const float izn = __frcp_rn(zn), izf = __frcp_rn(zf);  // (a few ulp: far inside the 2 px margin)
+  const float u0 = fx * fminf((x - rad) * izn, (x - rad) * izf) + cx - 2.f;
+  const float u1 = fx * fmaxf((x + rad) * izn, (x + rad) * izf) + cx + 2.f;
+  const float v0 = fy * fminf((y - rad) * izn, (y - rad) * izf) + cy - 2.f;
+  const float v1 = fy * fmaxf((y + rad) * izn, (y + rad) * izf) + cy + 2.f;
+  if (!(u1 >= -0.5f && v1 >= -0.5f && u0 < (float)K.W && v0 < (float)K.H)) return kCull;
+  const bool inside = u0 >= 0.f && v0 >= 0.f && u1 < (float)K.W - 1.f && v1 < (float)K.H - 1.f;
   const int pu0 = max(0, (int)floorf(u0 + 0.5f)), pu1 = min(K.W - 1, (int)floorf(u1 + 0.5f));
   const int pv0 = max(0, (int)floorf(v0 + 0.5f)), pv1 = min(K.H - 1, (int)floorf(v1 + 0.5f));
-  f.t0x = pu0 / kTile; f.t1x = pu1 / kTile; f.t0y = pv0 / kTile; f.t1y = pv1 / kTile;
-  f.lvl = tiles;
-  f.stride = ntx;
-  f.zn = zn;
-  f.verdict = 2;
-  if ((f.t1x - f.t0x + 1) * (f.t1y - f.t0y + 1) > 64) {  // large footprint: the coarse (8x8-tile) level
-    const int nty_f = (K.H + kTile - 1) / kTile;
-    f.lvl = tiles + ntx * nty_f;
-    f.stride = (ntx + 7) >> 3;
-    f.t0x >>= 3; f.t1x >>= 3; f.t0y >>= 3; f.t1y >>= 3;
-    if ((f.t1x - f.t0x + 1) * (f.t1y - f.t0y + 1) > max_tiles) f.verdict = 1;
+  int l = 0;
+  while (l < kLevels && ((pu1 >> (3 + l)) - (pu0 >> (3 + l)) > 3 || (pv1 >> (3 + l)) - (pv0 >> (3 + l)) > 3)) ++l;
+  if (l == kLevels) return kKeep;
+  const int s = 3 + l;
+  const uint2* lvl = tiles + P.off(l);
+  const int stride = P.nx(l), t0x = pu0 >> s, t1x = pu1 >> s, t0y = pv0 >> s, t1y = pv1 >> s;
+  uint2 m = make_uint2(0u, 0u);
+  if (lane16 < 0) {  // this thread alone: all 16 tiles (clamped into the footprint: repeats are harmless)
+    uint2 tv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tv[q] = __ldg(lvl + min(t0y + (q >> 2), t1y) * stride + min(t0x + (q & 3), t1x));
+#pragma unroll
+    for (int q = 0; q < 16; ++q) m = tmax(m, tv[q]);
+  } else {  // the warp (uniform box): lane q < 16 loads tile q
+    if (lane16 < 16) m = __ldg(lvl + min(t0y + (lane16 >> 2), t1y) * stride + min(t0x + (lane16 & 3), t1x));
+    for (int sft = 16; sft > 0; sft >>= 1)
+      m = tmax(m, make_uint2(__shfl_xor_sync(0xffffffffu, m.x, sft), __shfl_xor_sync(0xffffffffu, m.y, sft)));
   }
-  return f;
-}
-
-__device__ __forceinline__ bool footprint_keep(const Geom& g, const Intr& K, const Footprint& f, uint32_t m) {
-  if (m == 0) return false;
-  const float dmax = (float)((double)m * K.unit);
-  return f.zn - 1e-3f < dmax + (float)g.trunc;
-}
-
-__device__ __forceinline__ bool box_visible(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
-                                            const uint32_t* __restrict__ tiles, int ntx, double cxw, double cyw,
-                                            double czw, float rad, int max_tiles) {
-  const Footprint f = box_footprint(K, Tdev, tiles, ntx, cxw, cyw, czw, rad, max_tiles);
-  if (f.verdict != 2) return f.verdict == 1;
-  uint32_t m = 0;
-  for (int ty = f.t0y; ty <= f.t1y; ++ty)
-    for (int tx = f.t0x; tx <= f.t1x; ++tx) m = max(m, __ldg(f.lvl + ty * f.stride + tx));
-  return footprint_keep(g, K, f, m);
+  if (m.x == 0) return kCull;  // no valid pixel
+  if (!(zn - 1e-3f < (float)((double)m.x * K.unit) + (float)g.trunc)) return kCull;
+  const uint32_t mn = ~m.y;      // min raw over the tiles, 0 if any pixel is invalid
+  if (inside && mn != 0 && (float)((double)mn * K.unit) - (zf + 1e-3f) >= (float)g.trunc) return kFree;
+  return kKeep;
 }
 
 // Kept-brick list entries carry the brick coordinates packed 10:10:10 bits (grids up to 4096
-// voxels per axis, checked at volume creation), so the sweep decodes them with shifts instead of
-// two runtime integer divisions per thread.
+// voxels per axis, checked at volume creation) and the FREE class in bit 31, so the sweep decodes
+// them with shifts instead of two runtime integer divisions per thread.
+constexpr uint32_t kFreeBit = 1u << 31;
 __device__ __forceinline__ uint32_t pack_brick(int bx, int by, int bz) {
   return ((uint32_t)bz << 20) | ((uint32_t)by << 10) | (uint32_t)bx;
 }
@@ -210,75 +325,100 @@ __device__ __forceinline__ void append_warp(bool keep, uint32_t v, uint32_t* __r
   }
 }
 
-constexpr int kSuper = 8;  // super-brick = 8^3 bricks = 32^3 voxels
+constexpr int kSuper = 4;  // super-brick = 4^3 bricks = 16^3 voxels
 
-// Level 1: one warp per super-brick; the lanes share the footprint's tile loads.
-__global__ void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev, const uint32_t* __restrict__ tiles,
-                             int ntx, int nsx, int nsy, int nsz, uint32_t* __restrict__ slist,
-                             uint32_t* __restrict__ scount) {
+// Level 1: one thread per super-brick (its 16 tile loads issued together); survivors appended
+// warp-aggregated.
+__global__ __launch_bounds__(256) void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev,
+                                                    const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy, int nsz,
+                                                    uint32_t* __restrict__ slist, uint32_t* __restrict__ scount) {
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
-  const uint32_t sb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  if (sb >= ns) return;
-  const int sx = (int)(sb % (uint32_t)nsx);
-  const uint32_t r = sb / (uint32_t)nsx;
-  const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
-  // voxel-centre box of the super-brick: voxels [32 s, 32 s + 31] per axis
-  const double h = 16.0;
-  const Footprint f = box_footprint(K, Tdev, tiles, ntx, g.ox + g.voxel * (32.0 * sx + h), g.oy + g.voxel * (32.0 * sy + h),
-                                    g.oz + g.voxel * (32.0 * sz + h), (float)(15.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
-  bool keep = f.verdict == 1;
-  if (f.verdict == 2) {
-    const int nx = f.t1x - f.t0x + 1, nt = nx * (f.t1y - f.t0y + 1);
-    uint32_t m = 0;
-    for (int t = lane; t < nt; t += 32) m = max(m, __ldg(f.lvl + (f.t0y + t / nx) * f.stride + f.t0x + t % nx));
-    for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
-    keep = footprint_keep(g, K, f, m);
+  const uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x;
+  int c = kCull;
+  if (sb < ns) {
+    const int sx = (int)(sb % (uint32_t)nsx);
+    const uint32_t r = sb / (uint32_t)nsx;
+    const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
+    // voxel-centre box of the super-brick: voxels [16 s, 16 s + 15] per axis
+    c = box_class(g, K, Tdev, tiles, P, g.ox + g.voxel * (16.0 * sx + 8.0), g.oy + g.voxel * (16.0 * sy + 8.0),
+                  g.oz + g.voxel * (16.0 * sz + 8.0), (float)(7.5 * 1.7320508 * g.voxel) + 1e-3f, -1);
   }
-  if (lane == 0 && keep) slist[atomicAdd(scount, 1u)] = sb;
+  append_warp(c != kCull, sb, slist, scount);
 }
 
-// Level 2: the 512 bricks of every surviving super-brick (one CTA of 512 threads per super-brick).
-__global__ __launch_bounds__(512) void k_cull_bricks(Geom g, Intr K, const double* __restrict__ Tdev,
-                                                     const uint32_t* __restrict__ tiles, int ntx, int nsx, int nsy,
+// Level 2: one warp per surviving super-brick, two of its 64 bricks per lane; warp-stride loop over
+// the survivors with a grid of co-resident CTAs.
+__global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const double* __restrict__ Tdev,
+                                                     const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy,
                                                      const uint32_t* __restrict__ slist,
                                                      const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
                                                      uint32_t* __restrict__ count) {
   const uint32_t n = *scount;
-  const int t = threadIdx.x;
-  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < n; li += nw) {
     const uint32_t sb = slist[li];
     const int sx = (int)(sb % (uint32_t)nsx);
     const uint32_t r = sb / (uint32_t)nsx;
     const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
-    const int bx = sx * kSuper + (t & 7), by = sy * kSuper + ((t >> 3) & 7), bz = sz * kSuper + (t >> 6);
-    bool keep = false;
-    if (bx < g.nbx && by < g.nby && bz < g.nbz)
-      keep = box_visible(g, K, Tdev, tiles, ntx, g.ox + g.voxel * (4.0 * bx + 2.0), g.oy + g.voxel * (4.0 * by + 2.0),
-                         g.oz + g.voxel * (4.0 * bz + 2.0), (float)(1.5 * 1.7320508 * g.voxel) + 1e-3f, 64);
-    append_warp(keep, pack_brick(bx, by, bz), list, count);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = lane + 32 * h;
+      const int bx = sx * kSuper + (t & 3), by = sy * kSuper + ((t >> 2) & 3), bz = sz * kSuper + (t >> 4);
+      int c = kCull;
+      if (bx < g.nbx && by < g.nby && bz < g.nbz)
+        c = box_class(g, K, Tdev, tiles, P, g.ox + g.voxel * (4.0 * bx + 2.0), g.oy + g.voxel * (4.0 * by + 2.0),
+                      g.oz + g.voxel * (4.0 * bz + 2.0), (float)(1.5 * 1.7320508 * g.voxel) + 1e-3f, -1);
+      append_warp(c != kCull, pack_brick(bx, by, bz) | (c == kFree ? kFreeBit : 0u), list, count);
+    }
   }
 }
 
-// Sweep of the compacted bricks: 4 bricks per 256-thread CTA, grid-stride over the list.
+// A FREE-class voxel (box_class): v_new = 1, so V' = (V W + 1)/(W + 1) (= 1 exactly when V = 1, see
+// fuse_voxel) and W' = min(W + 1, W_max), each rounded once -- the oracle's update without its
+// projection, whose every possible outcome was proven to be "updated with v_new = 1".
+template <typename T>
+__device__ __forceinline__ bool fuse_free(const Geom& g, T Vs, T Ws, T* __restrict__ V, T* __restrict__ W, uint32_t o) {
+  const double Vo = to_double<T>(Vs), Wo = to_double<T>(Ws);
+  const double Wp = __dadd_rn(Wo, 1.0);
+  const double Wn = Wp > g.max_weight ? g.max_weight : Wp;
+  W[o] = store_rn<T>(Wn);
+  if (Vo == 1.0 && Wo >= 0.0 && Wo <= 1e300) return false;  // V' = 1: bits unchanged, not stored
+  const T Vnew = store_rn<T>(__ddiv_rn(__dadd_rn(__dmul_rn(Vo, Wo), 1.0), Wp));
+  V[o] = Vnew;
+  return !same_bits<T>(Vs, Vnew);
+}
+
+// Sweep of the compacted bricks: a warp covers half a brick (one voxel per lane), 4 bricks per
+// 256-thread CTA and iteration, CTA-stride over the list.  The next brick's list entry is loaded one
+// iteration ahead and the voxel's stored value/weight before the projection chain (their addresses
+// depend only on the list).
 template <typename T>
 __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const uint16_t* __restrict__ depth,
-                                                        const double* __restrict__ Tdev, const uint32_t* __restrict__ list,
+                                                        const double4* __restrict__ tab, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, T* __restrict__ V,
                                                         T* __restrict__ W, uint32_t* __restrict__ dirty,
                                                         uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount) {
-  __shared__ double sT[12];
-  if (threadIdx.x < 12) sT[threadIdx.x] = Tdev[threadIdx.x];
-  __syncthreads();
+  const int n0 = 4 * g.nbx, n1 = 4 * g.nby;
   const uint32_t n = *count;
   const uint32_t w = threadIdx.x & 63;
-  for (uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6); li < n; li += gridDim.x * 4) {
-    const uint32_t e = list[li];
-    const int bx = (int)(e & 1023u), by = (int)((e >> 10) & 1023u), bz = (int)(e >> 20);
+  const uint32_t step = gridDim.x * 4;
+  uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6);
+  uint32_t e = li < n ? __ldg(list + li) : 0u;
+  for (; li < n; li += step) {
+    const int bx = (int)(e & 1023u), by = (int)((e >> 10) & 1023u), bz = (int)((e >> 20) & 1023u);
+    const bool free_class = (e & kFreeBit) != 0u;  // brick-uniform
+    if (li + step < n) e = __ldg(list + li + step);  // the next brick's entry, in flight during this one
     const uint32_t b = ((uint32_t)bz * g.nby + (uint32_t)by) * g.nbx + (uint32_t)bx;
     const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
     bool changed = false;
-    if (i < g.nx && j < g.ny && k < g.nz) changed = fuse_voxel<T>(g, K, depth, sT, i, j, k, V, W, b * 64u + w);
+    if (i < g.nx && j < g.ny && k < g.nz) {
+      const uint32_t o = b * 64u + w;
+      const T Vs = V[o], Ws = W[o];  // issued first: independent of the projection chain
+      changed = free_class ? fuse_free<T>(g, Vs, Ws, V, W, o)
+                           : fuse_voxel<T>(g, K, depth, ld_axis(tab + i), ld_axis(tab + n0 + j),
+                                           ld_axis(tab + n0 + n1 + k), Vs, Ws, V, W, o);
+    }
     // cell-bricks whose records read this voxel: (b - d) for d in {0,1}^3, the -1 neighbours
     // only from the brick's low faces
     unsigned nbm = 0u;
@@ -289,55 +429,79 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
         if ((!(q & 1) || ex) && (!(q & 2) || ey) && (!(q & 4) || ez)) nbm |= 1u << q;
     }
     nbm = __reduce_or_sync(0xffffffffu, nbm);
-    if ((threadIdx.x & 31) == 0 && nbm) mark_dirty_cells(g, bx, by, bz, nbm, dirty, dlist, dcount);
+    if (nbm) mark_dirty_cells_warp(g, bx, by, bz, nbm, dirty, dlist, dcount);  // warp-uniform
   }
+}
+
+// Co-resident CTAs of `kern` at `threads` per CTA on the current device (cached per kernel and device).
+template <typename K>
+static int resident_grid(K kern, int threads) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<const void*, int> key((const void*)kern, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& c : cache)
+    if (c.first == key) return c.second;
+  int per_sm = 0, sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0);
+  const int v = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  cache.push_back({key, v});
+  return v;
 }
 
 pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intrinsics* Kp, const double* T,
                           int full_sweep, cudaStream_t st) {
-  Intr K{Kp->fx, Kp->fy, Kp->cx, Kp->cy, Kp->depth_unit_m, Kp->width, Kp->height};
+  Intr K{Kp->fx, Kp->fy, Kp->cx, Kp->cy, Kp->depth_unit_m, Kp->width, Kp->height,
+         fabs(Kp->cx) < 524288.0 && fabs(Kp->cy) < 524288.0};
   const Geom& g = vol->g;
-  const int ntx = (K.W + kTile - 1) / kTile, nty = (K.H + kTile - 1) / kTile;
-  const size_t ntiles_all = (size_t)ntx * nty + (size_t)((ntx + 7) >> 3) * ((nty + 7) >> 3);
-  if (ntiles_all * 4 > vol->L.tiles_bytes) full_sweep = 1;
+  const Pyr P = make_pyr(K.W, K.H);
+  if ((size_t)P.total * sizeof(uint2) > vol->L.tiles_bytes) full_sweep = 1;
+  double4* tab = (double4*)(vol->base + vol->L.axis_off);
   if (full_sweep) {
+    const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
+    PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<ntab, 256, 0, st>>>(K, g.max_depth, depth, nullptr, P, 0, g, T, tab));
     size_t n = vol->L.elems;
     size_t blocks = (n + 255) / 256;
     int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
     if (vol->esize == 4)
-      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<float><<<grid, 256, 0, st>>>(g, K, depth, T, (float*)(vol->base + vol->L.v_off),
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<float><<<grid, 256, 0, st>>>(g, K, depth, tab, (float*)(vol->base + vol->L.v_off),
                                                      (float*)(vol->base + vol->L.w_off), n));
     else
-      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<__half><<<grid, 256, 0, st>>>(g, K, depth, T, (__half*)(vol->base + vol->L.v_off),
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<__half><<<grid, 256, 0, st>>>(g, K, depth, tab, (__half*)(vol->base + vol->L.v_off),
                                                       (__half*)(vol->base + vol->L.w_off), n));
     records_rebuild_all(vol, st);
     return cuda_check("integrate (full sweep)");
   }
-  uint32_t* tiles = (uint32_t*)(vol->base + vol->L.tiles_off);
+  uint2* tiles = (uint2*)(vol->base + vol->L.tiles_off);
   uint32_t* list = (uint32_t*)(vol->base + vol->L.list_off);
   uint32_t* count = (uint32_t*)(vol->base + vol->L.scratch_off + 64);
   uint32_t* dcount = (uint32_t*)(vol->base + vol->L.scratch_off + 128);
   uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
   uint32_t* dlist = (uint32_t*)(vol->base + vol->L.dlist_off);
   cudaMemsetAsync(count, 0, 192, st);  // active, dirty and super-brick counts (scratch +64..+255)
-  cudaMemsetAsync(tiles + (size_t)ntx * nty, 0, 4 * (size_t)((ntx + 7) >> 3) * ((nty + 7) >> 3), st);  // coarse level
+  cudaMemsetAsync(tiles + P.off(4), 0, sizeof(uint2) * (size_t)(P.total - P.off(4)), st);  // levels 4-5 (atomicMax targets)
   {
-    dim3 blk(32, 8);
-    int nt = ntx * nty;
-    PFT_LAUNCH(PFT_PROF_CULL, st, k_depth_tiles<<<(nt + 7) / 8, blk, 0, st>>>(K, g.max_depth, depth, tiles, ntx, nty));
+    const int nreg = P.nx(3) * P.ny(3);
+    const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
+    PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<nreg + ntab, 256, 0, st>>>(K, g.max_depth, depth, tiles, P, nreg, g, T, tab));
   }
   const int nsx = (g.nbx + kSuper - 1) / kSuper, nsy = (g.nby + kSuper - 1) / kSuper, nsz = (g.nbz + kSuper - 1) / kSuper;
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
   uint32_t* slist = (uint32_t*)(vol->base + vol->L.slist_off);
   uint32_t* scount = (uint32_t*)(vol->base + vol->L.scratch_off + 192);
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns * 32 + 255) / 256, 256, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, nsz, slist, scount));
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<148 * 4, 512, 0, st>>>(g, K, T, tiles, ntx, nsx, nsy, slist, scount, list, count));
-  const int grid = 148 * 8;
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, nsz, slist, scount));
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count));
+  // grid = the resident capacity (one wave: no partial second wave of CTAs, the CTA-stride loop
+  // balances the bricks)
+  const int grid = vol->esize == 4 ? resident_grid(k_integrate_list<float>, 256) : resident_grid(k_integrate_list<__half>, 256);
   if (vol->esize == 4)
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (float*)(vol->base + vol->L.v_off),
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (float*)(vol->base + vol->L.v_off),
                                                   (float*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
   else
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, T, list, count, (__half*)(vol->base + vol->L.v_off),
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (__half*)(vol->base + vol->L.v_off),
                                                    (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
   records_rebuild_dirty(vol, st);
   return cuda_check("integrate");

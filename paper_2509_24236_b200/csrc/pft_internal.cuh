@@ -48,6 +48,7 @@ struct VolLayout {
   size_t dirty_off, dlist_off;        // records: dirty flag per cell-brick + dirty list (uint32 each)
   size_t slist_off;                   // integration: surviving super-bricks (8^3 bricks) list
   size_t tiles_off, tiles_bytes;      // integration: per-tile depth max (float)
+  size_t axis_off;                    // integration: per-frame axis tables, 4*(nbx+nby+nbz) double4
   size_t total;
 };
 
@@ -157,17 +158,29 @@ void prof_end(int cls, cudaStream_t st, const char* what);
 // (cells [4b-1, 4b+3] per axis, i.e. every cell with a corner in the brick).
 void records_rebuild_all(pft_volume* vol, cudaStream_t st);
 void records_rebuild_dirty(pft_volume* vol, cudaStream_t st);
-// Marks (dedup'ed) the cell-bricks whose records depend on voxel (x,y,z) of brick (bx,by,bz):
-// cells [x-1, x] per axis.  Called by the fusion kernel for voxels whose stored V changed.
-__device__ __forceinline__ void mark_dirty_cells(const Geom& g, int bx, int by, int bz, unsigned nbmask,
-                                                 uint32_t* dirty, uint32_t* dlist, uint32_t* dcount) {
-  // nbmask bit (dz*4 + dy*2 + dx): cell-brick (bx-dx, by-dy, bz-dz) is affected
-  for (int i = 0; i < 8; ++i) {
-    if (!((nbmask >> i) & 1u)) continue;
-    const int cx = bx - (i & 1), cy = by - ((i >> 1) & 1), cz = bz - (i >> 2);
-    if (cx < 0 || cy < 0 || cz < 0) continue;
-    const uint32_t cb = ((uint32_t)cz * g.nby + (uint32_t)cy) * g.nbx + (uint32_t)cx;
-    if (atomicExch(dirty + cb, 1u) == 0u) dlist[atomicAdd(dcount, 1u)] = cb;
+// Marks (dedup'ed) the cell-bricks whose records depend on a changed voxel of brick (bx,by,bz):
+// nbmask bit (dz*4 + dy*2 + dx) = cell-brick (bx-dx, by-dy, bz-dz) is affected.  Called by a whole
+// warp (nbmask warp-uniform): lane q < 8 claims neighbour q (atomicExch on its dirty flag), then the
+// newly claimed ones are appended with one warp-aggregated atomicAdd -- two atomic round trips in
+// total instead of up to 8 serial pairs.
+__device__ __forceinline__ void mark_dirty_cells_warp(const Geom& g, int bx, int by, int bz, unsigned nbmask,
+                                                      uint32_t* dirty, uint32_t* dlist, uint32_t* dcount) {
+  const int q = threadIdx.x & 31;
+  bool mine = false;
+  uint32_t cb = 0;
+  if (q < 8 && ((nbmask >> q) & 1u)) {
+    const int cx = bx - (q & 1), cy = by - ((q >> 1) & 1), cz = bz - (q >> 2);
+    if (cx >= 0 && cy >= 0 && cz >= 0) {
+      cb = ((uint32_t)cz * g.nby + (uint32_t)cy) * g.nbx + (uint32_t)cx;
+      mine = atomicExch(dirty + cb, 1u) == 0u;
+    }
+  }
+  const unsigned ball = __ballot_sync(0xffffffffu, mine);
+  if (ball) {
+    uint32_t base = 0;
+    if (q == 0) base = atomicAdd(dcount, (uint32_t)__popc(ball));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (mine) dlist[base + __popc(ball & ((1u << q) - 1u))] = cb;
   }
 }
 #define PFT_LAUNCH(cls, st, ...)        \

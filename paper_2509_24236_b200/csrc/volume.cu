@@ -52,9 +52,13 @@ static pft_status make_layout(const pft_volume_desc* d, Geom* g, VolLayout* L, s
   L->m_off = off; off = align_up(off + nb * 8, 256);
   L->list_off = off; L->list_bytes = nb * 4; off = align_up(off + L->list_bytes, 256);
   L->dirty_off = off; off = align_up(off + nb * 4, 256);
-  L->slist_off = off; off = align_up(off + ((nb + 511) / 512 + 64) * 4 * 8, 256);  // super-brick list
+  {
+    const size_t nsup = (size_t)((g->nbx + 3) / 4) * ((g->nby + 3) / 4) * ((g->nbz + 3) / 4);  // 4^3-brick super-bricks
+    L->slist_off = off; off = align_up(off + (nsup + 64) * 4, 256);  // super-brick list
+  }
   L->dlist_off = off; off = align_up(off + nb * 4, 256);
   L->tiles_off = off; L->tiles_bytes = 64 * 1024 * 4; off = align_up(off + L->tiles_bytes, 256);
+  L->axis_off = off; off = align_up(off + 4 * (size_t)(g->nbx + g->nby + g->nbz) * 4 * sizeof(double), 256);
   L->total = off;
   return PFT_OK;
 }

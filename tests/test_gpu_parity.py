@@ -293,6 +293,41 @@ def test_integrate_room_bit_exact(pft, storage):
     vol_full.close()
 
 
+@pytest.mark.parametrize("voxel", [0.0625, 0.05])
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_integrate_grid_aligned_pixel_ties(pft, voxel, storage):
+    """Adversarial projection decisions (integrate.cu pixel_of): a camera at the world origin with
+    identity rotation looking along +z over voxel centres x = s(i - 24), z = s k, fx = fy = 60,
+    cx = cy = 31.5, so fx x / z + cx + 1/2 = 60 (i - 24)/k + 32 lands exactly on (s = 1/16, binary)
+    or within ulps of (s = 0.05) integer pixel boundaries for many voxels: the guarded reciprocal
+    path must hand every such voxel to the exact division and decide the same pixel as the oracle.
+    A frontal plane at 1.5 m, fused 3 times (free space carved to V = 1, then the V' = 1 shortcut),
+    culled and full sweep, against the oracle bit for bit."""
+    n = 48
+    desc = VolumeDesc(n, n, n, voxel, (-voxel * 24.5, -voxel * 24.5, -voxel * 0.5), 2.5 * voxel, storage=storage)
+    intr = Intrinsics(60.0, 60.0, 31.5, 31.5, 64, 64)
+    T0 = np.zeros((3, 4))
+    T0[:, :3] = np.eye(3)
+    depth = np.full((64, 64), 1500, dtype=np.uint16)
+    depth[:, :7] = 0            # an invalid band
+    depth[40:, 30:] = 2200      # a step
+    vol = gpu_volume(pft, desc)
+    vfull = gpu_volume(pft, desc)
+    ov = oracle.OracleVolume(desc)
+    for _ in range(3):
+        vol.integrate(T(depth), intr, T(T0))
+        vfull.integrate(T(depth), intr, T(T0), full_sweep=True)
+        ov.integrate(depth, intr, T0)
+    for v in (vol, vfull):
+        V, W = [x.cpu().numpy() for x in v.download()]
+        assert np.array_equal(storage_bits(V), storage_bits(ov.V)), \
+            f"{int((storage_bits(V) != storage_bits(ov.V)).sum())} voxel values differ"
+        assert np.array_equal(storage_bits(W), storage_bits(ov.W))
+    assert (ov.weights_f64() == 3).sum() > 5000
+    vol.close()
+    vfull.close()
+
+
 def test_upload_download_roundtrip_and_checksum(pft):
     desc = VolumeDesc(37, 18, 23, 0.05, (0.0, 0.0, 0.0), 0.2)   # ragged bricks on every axis
     st = Stream(11, 11)
