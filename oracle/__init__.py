@@ -73,6 +73,8 @@ def lib():
         _lib.ora_quat_to_R.argtypes = [P, P]
         _lib.ora_track.restype = C.c_int32
         _lib.ora_track.argtypes = [P, P, P, P, P, P, C.c_int32, P, P, P, P, P, P, P, C.c_int32]
+        _lib.ora_track_ex.restype = C.c_int32
+        _lib.ora_track_ex.argtypes = [P, P, P, P, P, P, C.c_int32, P, P, P, P, P, P, P, P, P, C.c_int32]
         _lib.ora_eval_poses.restype = C.c_int32
         _lib.ora_eval_poses.argtypes = [P, P, P, P, C.c_int32, C.c_double, P, C.c_int32, P, P, P, P, C.c_int32]
         _lib.ora_integrate.restype = C.c_int64
@@ -177,8 +179,11 @@ class OracleVolume:
         return int(lib().ora_integrate(_p(self.V), _p(self.W), C.byref(self.cdesc), _p(depth), C.byref(ci),
                                        _p(T), nthreads or default_threads()))
 
-    def track(self, depth, intr, T_init, pst, params, nthreads=None):
-        """O7/O8 -> dict(T, E, n, trace, N, margin)."""
+    def track(self, depth, intr, T_init, pst, params, nthreads=None, force=None):
+        """O7/O8 -> dict(T, E, n, trace, N, margin, emargin).  emargin[i]: iteration i's smallest
+        relative distance of a fitness decision to its threshold (inf for iterations not run);
+        force (iters x K int8, -1 = decide): the shadowed re-run with a given membership
+        (pft_oracle.c ora_track_ex)."""
         depth = np.ascontiguousarray(depth, dtype=np.uint16)
         T_init = np.ascontiguousarray(T_init, dtype=np.float64)
         pst = np.ascontiguousarray(pst, dtype=np.float32)
@@ -189,11 +194,16 @@ class OracleVolume:
         n = np.zeros(K, dtype=np.int32)
         tr = np.zeros((params.iters, TRACE_DOUBLES))
         m = np.ones(1)
+        em = np.full(params.iters, np.inf)
         ci, cp = make_intr(intr), make_params(params)
-        N = lib().ora_track(_p(self.V), C.byref(self.cdesc), _p(depth), C.byref(ci), _p(T_init), _p(pst), K,
-                            C.byref(cp), _p(ws), _p(T), _p(E), _p(n), _p(tr), _p(m),
-                            nthreads or default_threads())
-        return dict(T=T.reshape(3, 4), E=E, n=n, trace=tr, N=N, margin=float(m[0]))
+        fp = None
+        if force is not None:
+            force = np.ascontiguousarray(force, dtype=np.int8).reshape(params.iters, K)
+            fp = _p(force)
+        N = lib().ora_track_ex(_p(self.V), C.byref(self.cdesc), _p(depth), C.byref(ci), _p(T_init), _p(pst), K,
+                               C.byref(cp), _p(ws), _p(T), _p(E), _p(n), _p(tr), _p(m), _p(em), fp,
+                               nthreads or default_threads())
+        return dict(T=T.reshape(3, 4), E=E, n=n, trace=tr, N=N, margin=float(m[0]), emargin=em)
 
     def extract(self, max_pts=None):
         """F4 zero-crossing surface points (N x 3, canonical voxel/axis order)."""

@@ -282,10 +282,35 @@ void ora_apply_delta(const double dR[9], const double u[3], const double P[12], 
  * Returns N of the first iteration's point set (0: EMPTY_CLOUD semantics: P = T_init, E = 1, n = 0).
  * pts_ws must hold ceil(H/sy)*ceil(W/sx)*3 doubles for the densest point set used.  nthreads > 1
  * splits the independent particle evaluations across OpenMP threads (arithmetic unchanged). */
+int32_t ora_track_ex(const void *V, const ora_volume_desc *D, const uint16_t *depth,
+                     const ora_intrinsics *Kin, const double T_init[12], const float *pst, int32_t K,
+                     const ora_track_params *prm, double *pts_ws, double T_out[12], double *E_out,
+                     int32_t *n_out, double *trace, double *min_margin, double *emargin,
+                     const int8_t *force, int32_t nthreads);
+
+/* O7 with the parity protocol's bookkeeping off: see ora_track_ex. */
 int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth,
                   const ora_intrinsics *Kin, const double T_init[12], const float *pst, int32_t K,
                   const ora_track_params *prm, double *pts_ws, double T_out[12], double *E_out,
                   int32_t *n_out, double *trace, double *min_margin, int32_t nthreads) {
+  return ora_track_ex(V, D, depth, Kin, T_init, pst, K, prm, pts_ws, T_out, E_out, n_out, trace, min_margin,
+                      NULL, NULL, nthreads);
+}
+
+/* Margin-aware parity protocol, test bookkeeping around O7:
+ *   emargin (NULL or iters doubles): per iteration, the smallest relative distance of a decision on
+ *     fitness values to its threshold: min over k < K_i of |E_k - E_base|, for the top-k rule also
+ *     the gap between the topk-th and the next member, for the guard also |E(P') - E_base|; divided
+ *     by E_base (1 when E_base = 0).  A GPU/oracle difference in the advantage set is a "tie" only
+ *     where this is tiny.
+ *   force (NULL or iters x K int8): -1 = decide as defined; 0 / 1 = particle k is (not) selected
+ *     into the average of that iteration regardless (the "shadowed" re-run with the other side's
+ *     membership).  With force == NULL the arithmetic is exactly O7's. */
+int32_t ora_track_ex(const void *V, const ora_volume_desc *D, const uint16_t *depth,
+                     const ora_intrinsics *Kin, const double T_init[12], const float *pst, int32_t K,
+                     const ora_track_params *prm, double *pts_ws, double T_out[12], double *E_out,
+                     int32_t *n_out, double *trace, double *min_margin, double *emargin,
+                     const int8_t *force, int32_t nthreads) {
   double P[12];
   memcpy(P, T_init, sizeof P);
   double omega = prm->omega0_deg, v = prm->v0_cm;
@@ -351,9 +376,29 @@ int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth
         kcut = pk;
       }
     }
+    if (emargin) {
+      double em = INFINITY;
+      for (int32_t k = 0; k < Ki; ++k) {
+        double d = fabs(E_out[k] - Ebase);
+        if (d < em) em = d;
+      }
+      if (prm->update_rule == 2 && kcut < Ki) { /* the member just outside the top-k */
+        double ne = 2.0;
+        int32_t nk = Ki;
+        for (int32_t k = 0; k < Ki; ++k) {
+          double e = E_out[k];
+          if (!(e < Ebase) || e < Ecut || (e == Ecut && k <= kcut)) continue;
+          if (e < ne || (e == ne && k < nk)) { ne = e; nk = k; }
+        }
+        if (nk < Ki && ne - Ecut < em) em = ne - Ecut;
+      }
+      emargin[it] = em / (Ebase > 0.0 ? Ebase : 1.0);
+    }
     for (int32_t k = 0; k < Ki; ++k) {
-      if (E_out[k] < Ebase) {
-        if (prm->update_rule == 2 && kcut < Ki && (E_out[k] > Ecut || (E_out[k] == Ecut && k > kcut))) continue;
+      int sel = E_out[k] < Ebase;
+      if (sel && prm->update_rule == 2 && kcut < Ki && (E_out[k] > Ecut || (E_out[k] == Ecut && k > kcut))) sel = 0;
+      if (force && force[(size_t)it * K + k] >= 0) sel = force[(size_t)it * K + k];
+      if (sel) {
         double w = prm->update_rule == 1 ? Ebase - E_out[k] : 1.0;
         for (int j = 0; j < 4; ++j) Q[j] += w * q_all[4 * (size_t)k + j];
         for (int j = 0; j < 3; ++j) U[j] += w * u_all[3 * (size_t)k + j];
@@ -371,6 +416,10 @@ int32_t ora_track(const void *V, const ora_volume_desc *D, const uint16_t *depth
       ora_quat_to_R(qbar, Rbar);
       ora_apply_delta(Rbar, ubar, P, prm->delta_conv, Pn);
       double En = ora_fitness(V, D, pts_ws, N, Pn, prm->min_inband_frac, &ncn, min_margin);
+      if (emargin && prm->guard) {
+        double g = fabs(En - Ebase) / (Ebase > 0.0 ? Ebase : 1.0);
+        if (g < emargin[it]) emargin[it] = g;
+      }
       if (prm->guard && En > Ebase) {
         rejected = 1;
       } else {

@@ -8,9 +8,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 
-def main(cfg, seed, out):
-    import torch
-    import paper_2509_24236_b200 as pft
+def make_case(cfg, seed):
+    """(config dict, params) of a named case (shared with the tests that compare it to the oracle)."""
     from synth.configs import config_single, config_tiny, with_desc
     import dataclasses
     c = config_tiny(seed=seed) if cfg.startswith("tiny") else config_single(seed=seed)
@@ -24,11 +23,18 @@ def main(cfg, seed, out):
     if cfg == "tiny16":
         c = with_desc(c, storage="f16")
         c["V"], c["W"] = c["V"].astype(np.float16), c["W"].astype(np.float16)
+    return c, c["params"]
+
+
+def main(cfg, seed, out):
+    import torch
+    import paper_2509_24236_b200 as pft
+    c, params = make_case(cfg, seed)
     dev = torch.device("cuda", 0)
     vol = pft.Volume(c["desc"], dev)
     vol.upload(c["V"], c["W"])
     r = vol.track(torch.from_numpy(c["depth"]).to(dev), c["intr"], torch.from_numpy(c["T_init"]).to(dev),
-                  torch.from_numpy(c["pst"]).to(dev), c["params"])
+                  torch.from_numpy(c["pst"]).to(dev), params)
     torch.cuda.synchronize()
     np.savez(out, **{k: r[k].cpu().numpy() for k in ("T", "E", "n", "trace")})
 

@@ -6,13 +6,16 @@ the fusion arithmetic is evaluated in the same fp64 operation order on both side
 within 1e-4 m and 1e-4 rad.  A count mismatch is accepted only as a "tie": the oracle's cell
 decision margin (distance of a grid coordinate to an integer) below 1e-9 voxel units.
 """
+import dataclasses
+
 import numpy as np
 
 import oracle
 
 E_REL, E_ABS = 1e-5, 1e-9
 POSE_M, POSE_RAD = 1e-4, 1e-4
-TIE_MARGIN = 1e-9
+TIE_MARGIN = 1e-9   # cell decisions: distance of a grid coordinate to an integer (voxel units)
+E_TIE = 1e-8        # fitness decisions: relative distance of E_k to E_base (oracle emargin)
 
 
 def close_E(a, b):
@@ -70,8 +73,12 @@ def assert_last_iter_counts(n_gpu, E_gpu, o, ov, depth, intr, pst, params, T_ini
     bad = np.nonzero(n_gpu != o["n"])[0]
     if len(bad):
         tr = o["trace"]
-        P_last = tr[-2, 4:16].reshape(3, 4) if len(tr) > 1 else np.asarray(T_init).reshape(3, 4)
-        om, v = tr[-1, 2], tr[-1, 3]
+        # the last iteration that ran (rows after a stop rule are "not run", flag bit 5): its
+        # search size, and the pose it started from (the row before it, or T_init)
+        ran = [i for i in range(len(tr)) if not (int(tr[i, 19]) & 32)]
+        last = ran[-1]
+        P_last = tr[last - 1, 4:16].reshape(3, 4) if last > 0 else np.asarray(T_init).reshape(3, 4)
+        om, v = tr[last, 2], tr[last, 3]
         poses = []
         for k in bad:
             dR, _, u = oracle.delta(pst[k], om, v)
@@ -84,3 +91,79 @@ def assert_last_iter_counts(n_gpu, E_gpu, o, ov, depth, intr, pst, params, T_ini
     ok = close_E(E_gpu, o["E"]) | (n_gpu != o["n"])
     assert ok.all(), f"{what}: E mismatch at {np.nonzero(~ok)[0][:10]}"
     return len(bad)
+
+
+# ------------------------------------------------------------------ fitness-decision ties
+def selection(E, Ebase, Ki, params):
+    """The membership include/pft.h defines for one iteration, from that side's E_k and E_base:
+    A = {k < K_i : E_k < E_base}; for the top-k rule the topk smallest (E_k, k) of A."""
+    E = np.asarray(E, dtype=np.float64)
+    m = np.zeros(len(E), dtype=bool)
+    m[:Ki] = E[:Ki] < Ebase
+    if getattr(params, "update_rule", 0) == 2 and m.sum() > params.topk:
+        idx = np.nonzero(m)[0]
+        keep = idx[np.lexsort((idx, E[idx]))[:params.topk]]
+        m[:] = False
+        m[keep] = True
+    return m
+
+
+def first_selection_mismatch(tr_gpu, tr_ora):
+    """Index of the first run iteration whose |A| differs, or None."""
+    for i in range(tr_ora.shape[0]):
+        if int(tr_ora[i, 19]) & 32 or int(tr_gpu[i, 19]) & 32:
+            return None
+        if tr_gpu[i, 1] != tr_ora[i, 1]:
+            return i
+    return None
+
+
+def selection_margins(E, Ebase, Ki, params):
+    """Per particle k < K_i: the relative distance of E_k to the thresholds its selection depends on
+    (E_base; for the top-k rule also the topk-th and the next member's E)."""
+    E = np.asarray(E, dtype=np.float64)[:Ki]
+    m = np.abs(E - Ebase)
+    if getattr(params, "update_rule", 0) == 2:
+        mem = np.sort(E[E < Ebase])
+        if len(mem) > params.topk:
+            for c in (mem[params.topk - 1], mem[params.topk]):
+                m = np.minimum(m, np.abs(E - c))
+    return m / (Ebase if Ebase > 0 else 1.0)
+
+
+def track_parity(run_gpu, ov, depth, intr, T_init, pst, params, what="", max_ties=2):
+    """Whole-run parity with the margin-aware protocol.
+
+    run_gpu(iters) -> dict(T, E, n, trace) of the GPU path run with `iters` iterations (the API is
+    prefix-stable, include/pft.h).  The full GPU run is compared with the oracle; when the advantage
+    set first differs (iteration i), both sides' per-particle E_k of iteration i are taken from
+    prefix re-runs, and every particle whose selection differs must be a tie: its oracle E_k within
+    E_TIE (relative) of a threshold it is compared with.  The oracle is then re-run *shadowed* --
+    forced to the GPU's membership at i -- and everything downstream must agree again.  Returns
+    (gpu, oracle, number of tied iterations)."""
+    r = run_gpu(params.iters)
+    K = np.asarray(pst).shape[0]
+    force = np.full((params.iters, K), -1, dtype=np.int8)
+    o = ov.track(depth, intr, T_init, pst, params)
+    ties = 0
+    while True:
+        i = first_selection_mismatch(r["trace"], o["trace"])
+        if i is None:
+            break
+        assert ties < max_ties, f"{what}: more than {max_ties} tied iterations"
+        Ki = int(o["trace"][i, 22]) if o["trace"].shape[1] > 22 else K
+        ri = run_gpu(i + 1)
+        oi = ov.track(depth, intr, T_init, pst, dataclasses.replace(params, iters=i + 1), force=force[:i + 1])
+        m_gpu = selection(ri["E"], r["trace"][i, 0], Ki, params)
+        m_ora = selection(oi["E"], o["trace"][i, 0], Ki, params)
+        diff = np.nonzero(m_gpu[:Ki] != m_ora[:Ki])[0]
+        marg = selection_margins(oi["E"], o["trace"][i, 0], Ki, params)[diff]
+        assert len(diff) and np.all(marg < E_TIE), \
+            f"{what} iter {i + 1}: |A| gpu={r['trace'][i, 1]} oracle={o['trace'][i, 1]}; particles {diff[:8]} " \
+            f"differ with fitness margins {marg[:8]} (not a tie)"
+        force[i, :] = 0
+        force[i, :Ki] = m_gpu[:Ki]
+        o = ov.track(depth, intr, T_init, pst, params, force=force)
+        ties += 1
+    assert_trace_parity(r["trace"], o["trace"], what)
+    return r, o, ties

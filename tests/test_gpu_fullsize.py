@@ -1,6 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times:
 config W (512^3 fp32, K = 4096 full 10-iteration trace; K = 65536 sampled), config Q (512^3 fp32)
 and config L (1024^3 fp16) as short GPU/oracle lock-step sequences (track + integrate)."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -9,7 +11,7 @@ from synth.configs import Sequence, TrackParams, config_sweep, init_noise
 from synth.rng import Stream
 from synth.scene import compose, inverse
 from tests.parity import (assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
-                          close_E)
+                          close_E, track_parity)
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -39,19 +41,45 @@ def sweep():
     vol.close()
 
 
+_W4096 = {}
+
+
+def _w4096_oracle(c, ov):
+    """The oracle's config-W K = 4096 run (shared by the tests of the sharded paths)."""
+    if "o" not in _W4096:
+        _W4096["o"] = ov.track(c["depth"], c["intr"], c["T_init"], c["pst"][:4096].copy(), TrackParams(iters=10, stride=4))
+    return _W4096["o"]
+
+
+def _np(r):
+    return {k: r[k].cpu().numpy() for k in ("T", "E", "n", "trace")}
+
+
+def _w4096_vs_oracle(r, c, ov, what):
+    pst = c["pst"][:4096].copy()
+    params = TrackParams(iters=10, stride=4)
+    o = _w4096_oracle(c, ov)
+    assert_trace_parity(r["trace"], o["trace"], what)
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], pst, params, c["T_init"], what)
+    assert_pose_close(r["T"], o["T"], what)
+
+
 def test_sweep_W_k4096_full_trace(sweep):
     """Config W, K = 4096: the whole 10-iteration RO run, every iteration's |A|, E, s and pose and the
-    last iteration's per-particle E_k / n_k against the oracle."""
+    last iteration's per-particle E_k / n_k against the oracle (margin-aware: an advantage-set
+    difference must be a fitness tie, then the oracle is shadowed, tests/parity.py)."""
     c, vol, ov = sweep
     pst = c["pst"][:4096].copy()
     params = TrackParams(iters=10, stride=4)
-    r = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), T(pst), params)
-    torch.cuda.synchronize()
-    o = ov.track(c["depth"], c["intr"], c["T_init"], pst, params)
-    assert_trace_parity(r["trace"].cpu().numpy(), o["trace"], "W K=4096")
-    assert_last_iter_counts(r["n"].cpu().numpy(), r["E"].cpu().numpy(), o, ov, c["depth"], c["intr"], pst, params,
-                            c["T_init"], "W K=4096")
-    assert_pose_close(r["T"].cpu().numpy(), o["T"])
+
+    def run(iters):
+        p = TrackParams(iters=iters, stride=4)
+        r = vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), T(pst), p)
+        torch.cuda.synchronize()
+        return _np(r)
+    r, o, _ = track_parity(run, ov, c["depth"], c["intr"], c["T_init"], pst, params, "W K=4096")
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], pst, params, c["T_init"], "W K=4096")
+    assert_pose_close(r["T"], o["T"])
 
 
 def test_sweep_W_k65536_sampled(sweep):
@@ -79,7 +107,18 @@ def test_sweep_W_k65536_sampled(sweep):
     assert (n > 0).sum() > 1000
 
 
-def _lockstep(kind, n_frames, K, iters=10):
+def _ate_cm(traj, gt):
+    """ATE-RMSE in cm of the camera centres (no alignment; SPEC.md:98-115 raw variant)."""
+    d = np.array([np.linalg.norm(np.asarray(a)[:, 3] - np.asarray(g)[:, 3]) for a, g in zip(traj, gt)])
+    return float(np.sqrt(np.mean(d ** 2)) * 100.0)
+
+
+def _lockstep(kind, n_frames, K, check_frames, iters=10):
+    """GPU and oracle in lock step over the first n_frames of the sequence (SURVEY.md §8(c-4) item 5,
+    §8(d-6)): frame 0 fused at GT (L24); then per frame t, T_init = P_{t-1} (GT_{t-1}^-1 GT_t (+) noise)
+    -- config Q's chained network stand-in (L25) on the oracle's previous pose -- tracked by both
+    (whole-run parity, margin-aware), and both fuse the frame at the oracle's pose.  Voxel bits are
+    compared after the frames in check_frames; the ATE of both trajectories must agree."""
     import paper_2509_24236_b200 as pft
     seq = Sequence(kind, seed=1, n_frames=max(n_frames, 8), K=K, iters=iters)
     vol = pft.Volume(seq.desc, dev())
@@ -89,33 +128,50 @@ def _lockstep(kind, n_frames, K, iters=10):
     vol.integrate(T(d0), seq.intr, T(seq.gt[0]))
     ov.integrate(d0, seq.intr, seq.gt[0])
     P_prev = seq.gt[0]
+    traj_gpu, traj_ora = [seq.gt[0]], [seq.gt[0]]
+    ties = 0
+    pst_dev = T(seq.pst)
     for t in range(1, n_frames):
         depth = seq.depth(t)
         T_init = compose(P_prev, seq.rel_init(t))
-        r = vol.track(T(depth), seq.intr, T(T_init), T(seq.pst), seq.params)
-        torch.cuda.synchronize()
-        o = ov.track(depth, seq.intr, T_init, seq.pst, seq.params)
-        assert_trace_parity(r["trace"].cpu().numpy(), o["trace"], f"{kind} frame {t}")
-        assert_last_iter_counts(r["n"].cpu().numpy(), r["E"].cpu().numpy(), o, ov, depth, seq.intr, seq.pst,
-                                seq.params, T_init, f"{kind} frame {t}")
+        d_dev, ti_dev = T(depth), T(T_init)
+
+        def run(it):
+            r = vol.track(d_dev, seq.intr, ti_dev, pst_dev, dataclasses.replace(seq.params, iters=it))
+            torch.cuda.synchronize()
+            return {k: r[k].cpu().numpy() for k in ("T", "E", "n", "trace")}
+        r, o, nt = track_parity(run, ov, depth, seq.intr, T_init, seq.pst, seq.params, f"{kind} frame {t}")
+        ties += nt
+        assert_last_iter_counts(r["n"], r["E"], o, ov, depth, seq.intr, seq.pst, seq.params, T_init, f"{kind} frame {t}")
+        assert_pose_close(r["T"], o["T"], f"{kind} frame {t}")
+        traj_gpu.append(r["T"])
+        traj_ora.append(o["T"])
         P_prev = o["T"]
         # both sides fuse at the same (oracle) pose; the GPU pose is within 1e-4 of it
-        vol.integrate(T(depth), seq.intr, T(P_prev))
+        vol.integrate(d_dev, seq.intr, T(P_prev))
         ov.integrate(depth, seq.intr, P_prev)
-    V, W = [x.cpu().numpy() for x in vol.download()]
-    assert np.array_equal(bits(V), bits(ov.V)), f"{kind}: {int((bits(V) != bits(ov.V)).sum())} values differ"
-    assert np.array_equal(bits(W), bits(ov.W))
+        if t in check_frames:
+            V, W = [x.cpu().numpy() for x in vol.download()]
+            assert np.array_equal(bits(V), bits(ov.V)), f"{kind} frame {t}: {int((bits(V) != bits(ov.V)).sum())} values differ"
+            assert np.array_equal(bits(W), bits(ov.W)), f"{kind} frame {t}: weights differ"
+            del V, W
+    gt = [seq.gt[t] for t in range(n_frames)]
+    ate_gpu, ate_ora = _ate_cm(traj_gpu, gt), _ate_cm(traj_ora, gt)
+    assert abs(ate_gpu - ate_ora) <= 1e-2, f"{kind}: ATE gpu {ate_gpu:.6f} cm vs oracle {ate_ora:.6f} cm"  # 1e-4 m
     vol.close()
+    return dict(ate_gpu_cm=ate_gpu, ate_oracle_cm=ate_ora, ties=ties)
 
 
 def test_sequence_Q_512_lockstep():
-    """Config Q geometry: 512^3 @ 1 cm fp32, K = 2048, 10 iterations, 640x480 frames."""
-    _lockstep("Q", 3, 2048)
+    """Config Q: 512^3 @ 1 cm fp32, K = 2048, 10 iterations, 640x480 frames, the first 31 frames
+    (30 tracked) with the chained L25 init; voxel bits at frames 1, 2, 10 and 30; ATE of both."""
+    _lockstep("Q", 31, 2048, check_frames={1, 2, 10, 30})
 
 
 def test_sequence_L_1024_fp16_lockstep():
-    """Config L: 1024^3 @ 5 mm, tau 2 cm, fp16 values and weights (bit-exact fp16 rounding), K = 4096."""
-    _lockstep("L", 3, 4096)
+    """Config L: 1024^3 @ 5 mm, tau 2 cm, fp16 values and weights (bit-exact fp16 rounding), K = 4096,
+    the first 6 frames (5 tracked); voxel bits at frames 1, 2 and 5; ATE of both."""
+    _lockstep("L", 6, 4096, check_frames={1, 2, 5})
 
 
 def test_sweep_W_k4096_fused_exchange_G8(sweep):
@@ -132,8 +188,10 @@ def test_sweep_W_k4096_fused_exchange_G8(sweep):
     v8.comm_init_virtual(8, fused=True)
     b = v8.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
     torch.cuda.synchronize()
+    b = _np(b)
     for k in ("T", "E", "n", "trace"):
-        assert np.array_equal(a[k], b[k].cpu().numpy()), k
+        assert np.array_equal(a[k], b[k]), k
+    _w4096_vs_oracle(b, c, ov, "W K=4096 fused exchange G=8")
     v8.close()
 
 
@@ -211,6 +269,8 @@ def test_sweep_W_k4096_virtual_shards_G4(sweep):
     v4.comm_init_virtual(4)
     b = v4.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params)
     torch.cuda.synchronize()
+    b = _np(b)
     for k in ("T", "E", "n", "trace"):
-        assert np.array_equal(a[k], b[k].cpu().numpy()), k
+        assert np.array_equal(a[k], b[k]), k
+    _w4096_vs_oracle(b, c, ov, "W K=4096 virtual shards G=4")
     v4.close()

@@ -12,7 +12,7 @@ from synth.rng import Stream
 from synth.scene import Intrinsics, analytic_fill, box_room, perturb, render_depth
 from tests.fixtures import f_track_inputs, golden
 from tests.parity import (assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
-                          close_E)
+                          close_E, track_parity)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -75,6 +75,27 @@ def test_f_track_golden(pft):
     # and against the oracle
     o = oracle.OracleVolume(f["desc"], f["V"], f["W"]).track(f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
     assert_trace_parity(tr, o["trace"], "F-track")
+    vol.close()
+
+
+def test_f_mean_golden(pft):
+    """Fixture F-mean (tests/golden/f_mean.json): a two-member advantage set of non-coaxial
+    rotations; the GPU's averaged pose, E_k, |A|, E(P') and s against the hand-derived closed form
+    and the oracle."""
+    from tests.fixtures import f_mean_closed_form, f_mean_inputs
+    f = f_mean_inputs()
+    cf = f_mean_closed_form()
+    vol = gpu_volume(pft, f["desc"], f["V"], f["W"])
+    r = run_track(pft, vol, f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
+    tr = r["trace"][0]
+    assert tr[1] == 2
+    np.testing.assert_allclose(r["E"], cf["E"], atol=1e-7)
+    np.testing.assert_allclose(r["T"], cf["P"], atol=1e-12)
+    assert abs(tr[16] - cf["E_c"]) < 1e-7
+    assert abs(tr[17] - cf["s_next"][0]) < 2e-6
+    o = oracle.OracleVolume(f["desc"], f["V"], f["W"]).track(f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
+    assert_trace_parity(r["trace"], o["trace"], "F-mean")
+    np.testing.assert_array_equal(r["n"], o["n"])
     vol.close()
 
 
@@ -176,6 +197,30 @@ def test_track_tiny(pft, conv):
     assert close_E(r["E"], o["E"]).all()
     assert_pose_close(r["T"], o["T"], "tiny final")
     assert np.all(r["trace"][:, 21] == 4800)
+    vol.close()
+
+
+@pytest.mark.parametrize("variant", ["plain", "schedule", "high"])
+def test_track_min_inband_fraction(pft, variant):
+    """Reading L6 with rho = min_inband_frac > 0 through pft_track: E = 1 for a candidate whose
+    in-band count is below rho N -- plain, with the F1 schedule (N changes per point set), and a rho
+    high enough that many candidates (and some centres) are rejected -- every trace row and the last
+    E_k / n_k against the oracle."""
+    import dataclasses
+    c = config_tiny(seed=2)
+    base = TrackParams(iters=5, stride=1, min_inband_frac=0.3)
+    params = {"plain": base, "schedule": dataclasses.replace(base, **SCHED_TINY),
+              "high": dataclasses.replace(base, min_inband_frac=0.62)}[variant]
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    ov = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    r, o, _ = track_parity(lambda it: run_track(pft, vol, c["depth"], c["intr"], c["T_init"], c["pst"],
+                                                dataclasses.replace(params, iters=it)),
+                           ov, c["depth"], c["intr"], c["T_init"], c["pst"], params, f"rho {variant}")
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], c["pst"], params, c["T_init"], variant)
+    assert_pose_close(r["T"], o["T"], variant)
+    if variant == "high":  # the fraction rule really decides something here (|A| differs from rho = 0)
+        o0 = ov.track(c["depth"], c["intr"], c["T_init"], c["pst"], dataclasses.replace(params, min_inband_frac=0.0))
+        assert not np.array_equal(o0["trace"][:, 1], o["trace"][:, 1])
     vol.close()
 
 
@@ -395,6 +440,32 @@ def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
         outs[mode] = np.load(f)
     for k in ("T", "E", "n", "trace"):
         assert np.array_equal(outs["0"][k], outs["1"][k]), k
+    # and the multi-launch run (the G > 1 code path) against the oracle
+    from tests.helpers.run_track import make_case
+    c, params = make_case(cfg, 1)
+    _assert_vs_oracle(dict(outs["0"]), c, c["pst"], params, f"multi-launch {cfg}")
+
+
+_ORACLE_CACHE = {}
+
+
+def _oracle_run(key, c, pst, params):
+    """The oracle's run of a case (cached per key: the sharded tests compare several G with it)."""
+    if key not in _ORACLE_CACHE:
+        V, W = c["V"], c["W"]
+        if c["desc"].storage == "f16":
+            V, W = np.asarray(V).view(np.uint16), np.asarray(W).view(np.uint16)
+        ov = oracle.OracleVolume(c["desc"], V, W)
+        _ORACLE_CACHE[key] = (ov, ov.track(c["depth"], c["intr"], c["T_init"], pst, params))
+    return _ORACLE_CACHE[key]
+
+
+def _assert_vs_oracle(r, c, pst, params, what, key=None):
+    """Trace, last-iteration E_k / n_k and pose of a GPU run against the oracle (north_star bar)."""
+    ov, o = _oracle_run(key or what, c, pst, params)
+    assert_trace_parity(r["trace"], o["trace"], what)
+    assert_last_iter_counts(r["n"], r["E"], o, ov, c["depth"], c["intr"], pst, params, c["T_init"], what)
+    assert_pose_close(r["T"], o["T"], what)
 
 
 # ------------------------------------------------------------------ NEXT rows F1 / F3
@@ -513,6 +584,7 @@ def test_virtual_shards_bit_identical(pft, G):  # noqa: C901
         b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
         for k in ("T", "E", "n", "trace"):
             assert np.array_equal(a[k], b[k]), (name, G, k)
+        _assert_vs_oracle(b, c, pst, params, f"virtual shards G={G} {name}", key=name)
         vol.close()
 
 
@@ -551,6 +623,7 @@ def test_fused_exchange_bit_identical(pft, G):
         b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
         for k in ("T", "E", "n", "trace"):
             assert np.array_equal(a[k], b[k]), (name, G, k)
+        _assert_vs_oracle(b, c, pst, params, f"fused exchange G={G} {name}", key="fused " + name)
         # a second call on the same workspace: the exchange counters continue from the stored
         # round count (no reset handshake) and the results repeat
         b2 = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
@@ -591,3 +664,22 @@ def test_fused_exchange_counters_follow_the_layout(pft):
             assert np.array_equal(a[k], b[k]), (K, k)
     ref.close()
     vol.close()
+
+
+def test_debug_build_bounds_checked(tmp_path):
+    """The PFT_DEBUG build (every mask / record address bounds- and alignment-checked in the
+    evaluation, a trap on a bad one; DESIGN.md §9's stale-register hazard would show up here) runs
+    config S, a top-k run and the fp16 volume with results bit-identical to the product build."""
+    import subprocess
+    import sys
+    lib = str(tmp_path / "libpft_debug.so")
+    subprocess.check_call(["sh", os.path.join(ROOT, "paper_2509_24236_b200", "csrc", "build.sh"), lib, "-DPFT_DEBUG"])
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_track.py")
+    for cfg in ("single", "single_topk", "tiny16"):
+        outs = {}
+        for name, env in (("prod", dict(os.environ)), ("debug", dict(os.environ, PFT_LIB=lib))):
+            f = str(tmp_path / f"{cfg}_{name}.npz")
+            subprocess.check_call([sys.executable, helper, cfg, "1", f], env=env)
+            outs[name] = np.load(f)
+        for k in ("T", "E", "n", "trace"):
+            assert np.array_equal(outs["prod"][k], outs["debug"][k]), (cfg, k)

@@ -243,3 +243,24 @@ def test_topk_reductions_and_closed_form():
         Q, U = Q + q, U + u
     Pn = oracle.apply_delta(oracle.quat_to_R(Q / np.linalg.norm(Q)), U / 8, c["T_init"], 0)
     assert r8["trace"][0, 1] == 8 and np.abs(r8["T"] - Pn).max() < 1e-12
+
+
+def test_f_mean_non_coaxial_quaternion_average():
+    """O7 average over a two-member advantage set with non-coaxial rotations (rotX(10 deg) and
+    rotY(10 deg)) against the hand-derived axis-angle closed form (tests/golden/f_mean.json): pins
+    the L13 reading (normalised quaternion sum; a rotation-vector mean differs by 2.8e-5 rad), the
+    left-multiplied camera-centred composition and the sense of the rotation."""
+    from tests.fixtures import f_mean_closed_form, f_mean_inputs
+    f = f_mean_inputs()
+    cf = f_mean_closed_form()
+    o = oracle.OracleVolume(f["desc"], f["V"], f["W"]).track(f["depth"], f["intr"], f["T_init"], f["pst"], f["params"])
+    tr = o["trace"][0]
+    assert tr[1] == 2
+    assert abs(tr[0] - cf["E_base"]) < 1e-7
+    np.testing.assert_allclose(o["E"], cf["E"], atol=1e-7)
+    np.testing.assert_allclose(o["T"], cf["P"], atol=1e-12)
+    np.testing.assert_allclose(tr[4:16].reshape(3, 4), cf["P"], atol=1e-12)
+    assert abs(tr[16] - cf["E_c"]) < 1e-7
+    assert abs(tr[17] - cf["s_next"][0]) < 2e-6 and abs(tr[18] - cf["s_next"][1]) < 1e-6
+    # the reading matters at this size: the rotation-vector mean is a different pose
+    assert abs(cf["phi"] - np.deg2rad(10.0) / np.sqrt(2.0)) > 2e-5
