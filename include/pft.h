@@ -166,6 +166,13 @@ pft_status pft_integrate(pft_volume* vol, const uint16_t* dev_depth, const pft_i
 pft_status pft_integrate_ex(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K,
                             const double* dev_T, int32_t flags, void* stream);
 
+/* Work counters of the last culled pft_integrate call on this volume (measurement):
+ * out[0] bricks kept by the cull (4^3 voxels each), out[1] of those classified free space (every
+ * voxel provably updated with v_new = 1, no projection), out[2] voxels updated (W or V written),
+ * out[3] cell-bricks whose tracker records were rebuilt.  Syncs `stream`.  After a full-sweep
+ * call the counters are not maintained (out[] = -1). */
+pft_status pft_integrate_stats(const pft_volume* vol, int64_t out[4], void* stream);
+
 /* NEXT F4: zero-crossing surface points, input of the completeness / accuracy
  * metrics of PAPER.md:562-563.  For every voxel and axis whose +1 neighbour is in the grid, both
  * observed (W > 0), values of different sign (not both 0): t = V0/(V0 - V1), point = voxel centre
@@ -223,6 +230,11 @@ pft_status pft_eval_poses(const pft_volume* vol, const uint16_t* dev_depth, cons
  * Syncs `stream`. */
 pft_status pft_track_info(const void* dev_ws, int32_t* npoints_out, void* stream);
 
+/* Device-side pose chaining (the sequence driver O11 / reading L25: T_init = P_{t-1} * rel_t):
+ * dev_out = dev_A * dev_B for rigid 3x4 row-major [R|t] poses, i.e. (R_A R_B, R_A t_B + t_A), in
+ * fp64 (dev_out may alias an input).  Enqueued on `stream`. */
+pft_status pft_pose_compose(const double* dev_A, const double* dev_B, double* dev_out, void* stream);
+
 /* ---------------------------------------------------------------- multi-GPU (north_star) */
 
 /* NCCL unique id for pft_comm_init (call on one rank, broadcast the 128 bytes). */
@@ -230,7 +242,10 @@ pft_status pft_comm_get_unique_id(uint8_t id_out[128]);
 
 /* Attaches an NCCL communicator (one rank per GPU) to the volume handle; afterwards
  * pft_track shards particles across the nranks GPUs.  The volume is replicated: every rank
- * calls pft_integrate with the same inputs.  The current CUDA device must be this rank's. */
+ * calls pft_integrate with the same inputs.  The current CUDA device must be this rank's.
+ * PFT_ERR_STATE if virtual ranks or peer exchange buffers are set on the handle.  Collective
+ * failures, including asynchronous ones (ncclCommGetAsyncError, polled after each collective),
+ * return PFT_ERR_NCCL. */
 pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks, int32_t rank);
 
 /* F2 fused exchange (Sec. III-C "Randomized optimization": every
@@ -242,7 +257,8 @@ pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks,
  * update -- no NCCL launch and no host round trip per iteration.  Counters are monotone across
  * calls (each rank stores the number of completed rounds in its own buffer), so calls need no
  * reset handshake; all ranks must call pft_track with the same arguments the same number of
- * times.  A rank that waits more than 5 s for a peer traps (launch error instead of a hang).
+ * times.  A rank that waits longer than the watchdog for a peer traps (a launch error instead of
+ * a hang; environment PFT_WATCHDOG_MS, default 5000, read once per process).
  *
  * pft_comm_p2p_init: allocates (cudaMalloc, zero-filled) this rank's exchange buffer sized for
  *   up to max_particles particles and nranks <= PFT_MAX_FUSED_RANKS ranks, and writes its
@@ -262,6 +278,22 @@ pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles);
  * the volume is then single-rank again (or keeps an attached NCCL communicator).  For a job
  * whose ranks could not all attach: every rank detaches and falls back to pft_comm_init. */
 pft_status pft_comm_p2p_detach(pft_volume* vol);
+/* Pre-flight of the attached peer exchange, before the first pft_track: one small kernel writes a
+ * token into every rank's buffer over NVLink (system-scope release stores) and waits, at most
+ * timeout_ms, for every peer's token in its own buffer (acquire loads).  *ok_out = 1 when all G
+ * arrived intact, 0 otherwise (no trap: the caller agrees with the other ranks and falls back to
+ * pft_comm_init).  All ranks must call it; syncs `stream`.  PFT_ERR_STATE if not attached. */
+pft_status pft_comm_p2p_preflight(pft_volume* vol, int32_t timeout_ms, int32_t* ok_out, void* stream);
+
+/* F2b (SURVEY.md §8(e) "alternative partition"): how pft_track splits the work across the ranks
+ * of an NCCL communicator (or virtual shards).  PARTICLES (default): rank r evaluates template rows
+ * [r*ceil(K/G), ...) on all points; the per-particle records are all-gathered.  POINTS: every rank
+ * evaluates all K_i particles on its contiguous slice of the strided point slots (whole 8x4 tiles),
+ * and the per-particle fixed-point sums -- and the centre's -- are summed by an integer all-reduce
+ * (exact, so results equal the 1-rank run bit for bit).  PFT_ERR_UNSUPPORTED with the peer exchange. */
+#define PFT_PARTITION_PARTICLES 0
+#define PFT_PARTITION_POINTS 1
+pft_status pft_comm_set_partition(pft_volume* vol, int32_t partition);
 
 /* ---------------------------------------------------------------- instrumentation */
 

@@ -5,4 +5,4 @@ This package is its thin Python binding.  It never imports the test oracle (orac
 """
 from ._lib import (EXPORTS, LIB_PATH, TRACE_DOUBLES, PftError, launch_count, lib, profile_start,  # noqa: F401
                    profile_stop)
-from .api import Volume, make_desc, make_intr, make_params, shard_range  # noqa: F401
+from .api import Volume, make_desc, make_intr, make_params, pose_compose, shard_range  # noqa: F401

@@ -19,10 +19,10 @@ STATUS = {0: "PFT_OK", -1: "PFT_ERR_INVALID_ARG", -2: "PFT_ERR_BUFFER_TOO_SMALL"
 
 # every symbol include/pft.h declares (checked by tests/test_abi.py)
 EXPORTS = ["pft_volume_bytes", "pft_volume_create", "pft_volume_reset", "pft_volume_upload", "pft_volume_download",
-           "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_extract_surface",
-           "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_comm_get_unique_id",
+           "pft_volume_checksum", "pft_volume_destroy", "pft_integrate", "pft_integrate_ex", "pft_integrate_stats", "pft_extract_surface",
+           "pft_track_workspace_bytes", "pft_track", "pft_eval_poses", "pft_track_info", "pft_pose_compose", "pft_comm_get_unique_id",
            "pft_comm_init", "pft_comm_init_virtual", "pft_comm_init_virtual_fused", "pft_comm_p2p_init",
-           "pft_comm_p2p_attach", "pft_comm_p2p_detach", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
+           "pft_comm_p2p_attach", "pft_comm_p2p_detach", "pft_comm_p2p_preflight", "pft_comm_set_partition", "pft_last_error", "pft_abi_version", "pft_launch_count", "pft_profile_start",
            "pft_profile_stop"]
 PROF_CLASSES = ["eval", "centre", "update", "prep", "integrate", "cull", "comm", "other", "records", "track"]
 
@@ -75,6 +75,7 @@ def lib():
         "pft_volume_destroy": [P],
         "pft_integrate": [P, P, P, P, P],
         "pft_integrate_ex": [P, P, P, P, I32, P],
+        "pft_integrate_stats": [P, P, P],
         "pft_extract_surface": [P, P, C.c_int64, P, P],
         "pft_track_workspace_bytes": [P, P, I32, P, P],
         "pft_track": [P, P, P, P, P, I32, P, P, SZ, P, P, P, P, P],
@@ -87,6 +88,9 @@ def lib():
         "pft_comm_p2p_init": [P, I32, I32, I32, P],
         "pft_comm_p2p_attach": [P, P],
         "pft_comm_p2p_detach": [P],
+        "pft_comm_p2p_preflight": [P, I32, P, P],
+        "pft_comm_set_partition": [P, I32],
+        "pft_pose_compose": [P, P, P, P],
         "pft_profile_start": [],
         "pft_profile_stop": [P, P],
     }

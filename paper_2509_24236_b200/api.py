@@ -113,6 +113,13 @@ class Volume:
         check(lib().pft_integrate_ex(self.handle, _vp(depth), C.byref(ci), _vp(T),
                                      INTEGRATE_FULL_SWEEP if full_sweep else 0, _stream(stream)))
 
+    def integrate_stats(self, stream=None):
+        """Work counters of the last culled integrate (include/pft.h pft_integrate_stats): dict of
+        kept bricks, free-space bricks, updated voxels, rebuilt cell-bricks.  Syncs."""
+        out = (C.c_int64 * 4)()
+        check(lib().pft_integrate_stats(self.handle, out, _stream(stream)))
+        return dict(kept_bricks=out[0], free_bricks=out[1], updated_voxels=out[2], dirty_cell_bricks=out[3])
+
     def extract_surface(self, max_points=None, stream=None):
         """F4 zero-crossing surface points -> (N, 3) fp64 device tensor (unordered)."""
         cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -197,11 +204,13 @@ class Volume:
         self.nranks, self.rank = int(nranks), 0
         self._ws = {}
 
-    def comm_init_p2p(self, max_particles, group=None):
+    def comm_init_p2p(self, max_particles, group=None, preflight_ms=2000):
         """F2 fused exchange over NVLink peer memory: allocate this rank's exchange buffer, gather
-        every rank's CUDA IPC handle over torch.distributed `group`, open the peers'.  All ranks
-        agree on the outcome (an all-reduce of a success flag): returns True when every rank is
-        attached; otherwise every rank has detached again and False is returned (use comm_init)."""
+        every rank's CUDA IPC handle over torch.distributed `group`, open the peers', then run the
+        pre-flight token exchange (include/pft.h pft_comm_p2p_preflight; no trap on failure).  All
+        ranks agree on the outcome (all-reduces of a success flag): returns True when every rank is
+        attached and every pre-flight succeeded; otherwise every rank has detached again and False
+        is returned (use comm_init)."""
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         h = (C.c_uint8 * IPC_HANDLE_BYTES)()
@@ -210,16 +219,24 @@ class Volume:
         if ok:
             raw = (C.c_uint8 * (IPC_HANDLE_BYTES * world))(*handles)
             ok = lib().pft_comm_p2p_attach(self.handle, raw) == 0
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32)
-        if dist.get_backend(group) == "nccl":
-            flag = flag.to(self.device)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
-        if int(flag.item()) != 1:
+        if not _all_ranks(ok, group, self.device):
+            check(lib().pft_comm_p2p_detach(self.handle))
+            return False
+        dist.barrier(group=group)
+        okp = C.c_int32(0)
+        ok = lib().pft_comm_p2p_preflight(self.handle, int(preflight_ms), C.byref(okp), _stream(None)) == 0
+        if not _all_ranks(ok and okp.value == 1, group, self.device):
             check(lib().pft_comm_p2p_detach(self.handle))
             return False
         self.nranks, self.rank = world, rank
         self._ws = {}
         return True
+
+    def set_partition(self, points):
+        """F2b: shard the points (True) or the particles (False, default) across the ranks of the
+        NCCL communicator / virtual shards (include/pft.h pft_comm_set_partition)."""
+        check(lib().pft_comm_set_partition(self.handle, 1 if points else 0))
+        self._ws = {}
 
     def comm_detach_p2p(self):
         """Undo comm_init_p2p on this rank (single-rank again)."""
@@ -237,6 +254,24 @@ class Volume:
             self.close()
         except Exception:
             pass
+
+
+def _all_ranks(ok, group, device):
+    """True iff `ok` holds on every rank of `group` (an all-reduce MIN of a flag)."""
+    import torch.distributed as dist
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32)
+    if dist.get_backend(group) == "nccl":
+        flag = flag.to(device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return int(flag.item()) == 1
+
+
+def pose_compose(A, B, out=None, stream=None):
+    """out = A * B for 3x4 rigid poses on the device (include/pft.h pft_pose_compose)."""
+    if out is None:
+        out = torch.empty(3, 4, dtype=torch.float64, device=A.device)
+    check(lib().pft_pose_compose(_vp(A), _vp(B), _vp(out), _stream(stream)))
+    return out
 
 
 def gather_handles(mine, group=None):

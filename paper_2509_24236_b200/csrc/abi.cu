@@ -101,6 +101,7 @@ struct Nccl {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
   decltype(&ncclCommGetAsyncError) asyncErr = nullptr;
 };
@@ -116,12 +117,24 @@ static Nccl* nccl() {
       n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
       n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
       n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+      n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
       n.errStr = (decltype(n.errStr))dlsym(h, "ncclGetErrorString");
       n.asyncErr = (decltype(n.asyncErr))dlsym(h, "ncclCommGetAsyncError");
-      if (n.getUniqueId && n.commInitRank && n.commDestroy && n.allGather && n.errStr) n.h = h;
+      if (n.getUniqueId && n.commInitRank && n.commDestroy && n.allGather && n.allReduce && n.errStr) n.h = h;
     }
   }
   return n.h ? &n : nullptr;
+}
+
+// Asynchronous NCCL failures (a peer died, a network error) surface through the communicator's
+// async error state, not through the enqueue call: polled after every collective, mapped to
+// PFT_ERR_NCCL (include/pft.h).
+static pft_status nccl_async_check(Nccl* n, pft_volume* vol, const char* what) {
+  if (!n->asyncErr) return PFT_OK;
+  ncclResult_t a = ncclSuccess;
+  if (n->asyncErr((ncclComm_t)vol->nccl_comm, &a) != ncclSuccess) return PFT_OK;
+  if (a != ncclSuccess && a != ncclInProgress) return fail(PFT_ERR_NCCL, "%s: asynchronous error %s", what, n->errStr(a));
+  return PFT_OK;
 }
 
 pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st) {
@@ -131,7 +144,18 @@ pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t 
   ncclResult_t r = n->allGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)vol->nccl_comm, st);
   prof_end(PFT_PROF_COMM, st, "ncclAllGather");
   if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclAllGather: %s", n->errStr(r));
-  return PFT_OK;
+  return nccl_async_check(n, vol, "ncclAllGather");
+}
+
+// In-place sum of `count` uint64 words over the ranks (point-sharded partition, F2b).
+pft_status comm_allreduce_u64(pft_volume* vol, void* buf, size_t count, cudaStream_t st) {
+  Nccl* n = nccl();
+  if (!n || !vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator not initialised");
+  prof_begin(PFT_PROF_COMM, st);
+  ncclResult_t r = n->allReduce(buf, buf, count, ncclUint64, ncclSum, (ncclComm_t)vol->nccl_comm, st);
+  prof_end(PFT_PROF_COMM, st, "ncclAllReduce");
+  if (r != ncclSuccess) return fail(PFT_ERR_NCCL, "ncclAllReduce: %s", n->errStr(r));
+  return nccl_async_check(n, vol, "ncclAllReduce");
 }
 
 }  // namespace pft
@@ -238,7 +262,9 @@ pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int3
   if (vol->nccl_comm || vol->virtual_ranks) return fail(PFT_ERR_STATE, "another communicator is attached");
   const size_t kloc = ((size_t)max_particles + nranks - 1) / nranks;
   const size_t rec = (2 * sizeof(pft::PartRec) * kloc * (size_t)nranks + 255) / 256 * 256;
-  const size_t bytes = rec + (pft::kMaxFusedRanks + 1) * sizeof(unsigned long long);
+  // records (2 halves), then kMaxFusedRanks round counters + the completed-round word, then
+  // kMaxFusedRanks preflight tokens (pft_comm_p2p_preflight)
+  const size_t bytes = rec + (2 * pft::kMaxFusedRanks + 1) * sizeof(unsigned long long);
   char* p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "exchange buffer (%zu B): %s", bytes, cudaGetErrorString(e));
@@ -296,10 +322,29 @@ pft_status pft_comm_p2p_attach(pft_volume* vol, const uint8_t* handles) {
   return PFT_OK;
 }
 
+pft_status pft_comm_p2p_preflight(pft_volume* vol, int32_t timeout_ms, int32_t* ok_out, void* stream) {
+  if (!vol || !ok_out) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  if (!vol->p2p) return fail(PFT_ERR_STATE, "peers are not attached (pft_comm_p2p_attach)");
+  if (timeout_ms < 1) return fail(PFT_ERR_INVALID_ARG, "timeout_ms must be >= 1");
+  return pft::p2p_preflight(vol, timeout_ms, ok_out, (cudaStream_t)stream);
+}
+
+pft_status pft_comm_set_partition(pft_volume* vol, int32_t partition) {
+  if (!vol) return fail(PFT_ERR_INVALID_ARG, "vol is NULL");
+  if (partition != PFT_PARTITION_PARTICLES && partition != PFT_PARTITION_POINTS)
+    return fail(PFT_ERR_INVALID_ARG, "bad partition %d", partition);
+  if (partition == PFT_PARTITION_POINTS && (vol->p2p || vol->virtual_fused))
+    return fail(PFT_ERR_UNSUPPORTED, "the point-sharded partition runs on the NCCL / virtual-shard path only");
+  vol->partition = partition;
+  return PFT_OK;
+}
+
 pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks, int32_t rank) {
   if (!vol || !id) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PFT_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
   if (vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator already initialised");
+  if (vol->virtual_ranks || vol->virtual_fused) return fail(PFT_ERR_STATE, "virtual ranks are set (pft_comm_init_virtual*)");
+  if (vol->p2p || vol->xown) return fail(PFT_ERR_STATE, "peer exchange buffers are attached (pft_comm_p2p_detach first)");
   if (nranks == 1) { vol->nranks = 1; vol->rank = 0; return PFT_OK; }
   Nccl* n = nccl();
   if (!n) return fail(PFT_ERR_NCCL, "libnccl.so.2 not loadable");

@@ -13,6 +13,7 @@
 // margins) compacts the 4^3 bricks that can contain an updated voxel; the fusion kernel then
 // sweeps only those bricks, 64 consecutive elements (one brick = 2 x 128 B lines per array
 // at fp32) per pair of warps, fully coalesced.  The full sweep is kept for verification.
+#include <cstring>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -46,7 +47,7 @@ __device__ __forceinline__ double i2d(int i) {  // 0 <= i < 2^31
 // floor(x) in its low word.
 __device__ __forceinline__ int floor_lo(double x) { return __double2loint(__dadd_rd(x, 6755399441055744.0)); }
 
-// Pixel index floor(u2) of u2 = RN(RN(RN(p / z) + c) + 1/2), the oracle's expression (p = RN(f x)),
+// Pixel index floor(u2) of u2 = RN(RN(RN(p / z) + c) + 1/2), the definition's expression (O9) (p = RN(f x)),
 // given rz = RN(1/z) shared by both image axes.  Fast path: qa = RN(p rz) differs from RN(p/z) by
 // at most 1.5 ulp, so for |qa| < 2^19 and |c| < 2^19 the approximate u2a is within 2^-30 of u2
 // (two more roundings of values < 2^21, ulp 2^-32 each); whenever the fraction of u2a is at least
@@ -70,12 +71,12 @@ __device__ __forceinline__ bool pixel_of(double p, double z, double rz, double c
   return (unsigned)pix < (unsigned)n;
 }
 
-// Per-frame axis tables (fusion step 1, computed by k_frame_prep).  The oracle's camera coordinates are
+// Per-frame axis tables (fusion step 1, computed by k_frame_prep).  The definition's camera coordinates (O9) are
 //   x = RN(RN(RN(R00 d0) + RN(R10 d1)) + RN(R20 d2)),  d_a = RN(g_a - t_a),  g_a = RN(o_a + RN(s RN(i_a + 1/2)))
 // (T = [R|t] row-major, so x pairs with T[0], T[4], T[8]; y with T[1], T[5], T[9]; z with T[2], T[6],
 // T[10]).  Each product depends on one axis index only, so the 9 rounded products are tabulated once
 // per frame per axis index, {RN(T[4a] d_a), RN(T[4a+1] d_a), RN(T[4a+2] d_a)} for axis a, and a voxel
-// needs 3 table loads and 6 additions in the oracle's order -- the same bits.
+// needs 3 table loads and 6 additions in the definition's order -- the same bits.
 __device__ __forceinline__ double4 ld_axis(const double4* p) {
   double4 v;
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
@@ -84,8 +85,8 @@ __device__ __forceinline__ double4 ld_axis(const double4* p) {
 
 // Vs, Ws: the voxel's stored value and weight, loaded by the caller ahead of the dependent chain
 // (their addresses depend on nothing computed here).  Returns true iff the stored value V changed
-// (its cell records must then be refreshed).  Stored bits equal the oracle's: every value that reaches storage (z, sdf, v_new, V', W') is
-// computed with the oracle's exact operations (x, y, z from the axis tables in its order); the
+// (its cell records must then be refreshed).  Stored bits equal those of the plain fp64 definition (O9): every value that reaches storage (z, sdf, v_new, V', W') is
+// computed with the exact operations of the definition (O9) (x, y, z from the axis tables in its order); the
 // projection only decides a pixel (pixel_of's guarded reciprocal), and two divisions are skipped
 // where their correctly rounded result is known exactly: v_new = 1 when sdf >= tau (then
 // sdf/tau >= 1, rounded >= 1, clamped to 1), and V' = 1 when V = 1 and v_new = 1 (numerator
@@ -94,7 +95,8 @@ __device__ __forceinline__ double4 ld_axis(const double4* p) {
 template <typename T>
 __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
                                            const double4& A, const double4& B, const double4& C, T Vs, T Ws,
-                                           T* __restrict__ V, T* __restrict__ W, uint32_t o) {
+                                           T* __restrict__ V, T* __restrict__ W, uint32_t o, bool& updated) {
+  updated = false;
   const double z = __dadd_rn(__dadd_rn(A.z, B.z), C.z);
   if (!(z > 0.0)) return false;
   const double x = __dadd_rn(__dadd_rn(A.x, B.x), C.x);
@@ -122,6 +124,7 @@ __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const u
   const T Vnew = store_rn<T>(Vn);
   V[o] = Vnew;
   W[o] = store_rn<T>(Wn);
+  updated = true;
   return !same_bits<T>(Vs, Vnew);
 }
 
@@ -138,8 +141,9 @@ __global__ __launch_bounds__(256) void k_integrate_sweep(Geom g, Intr K, const u
     const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);
     const int i = bx * 4 + (int)(w & 3), j = by * 4 + (int)((w >> 2) & 3), k = bz * 4 + (int)(w >> 4);
     if (i >= g.nx || j >= g.ny || k >= g.nz) continue;
+    bool updated;
     fuse_voxel<T>(g, K, depth, ld_axis(tab + i), ld_axis(tab + n0 + j), ld_axis(tab + n0 + n1 + k), V[e], W[e], V, W,
-                  (uint32_t)e);
+                  (uint32_t)e, updated);
   }
 }
 
@@ -352,7 +356,7 @@ __global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const doubl
                                                      const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy,
                                                      const uint32_t* __restrict__ slist,
                                                      const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
-                                                     uint32_t* __restrict__ count) {
+                                                     uint32_t* __restrict__ count, uint32_t* __restrict__ nfree_out) {
   const uint32_t n = *scount;
   const int lane = threadIdx.x & 31;
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -370,12 +374,14 @@ __global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const doubl
         c = box_class(g, K, Tdev, tiles, P, g.ox + g.voxel * (4.0 * bx + 2.0), g.oy + g.voxel * (4.0 * by + 2.0),
                       g.oz + g.voxel * (4.0 * bz + 2.0), (float)(1.5 * 1.7320508 * g.voxel) + 1e-3f, -1);
       append_warp(c != kCull, pack_brick(bx, by, bz) | (c == kFree ? kFreeBit : 0u), list, count);
+      const unsigned nfree = __popc(__ballot_sync(0xffffffffu, c == kFree));
+      if (lane == 0 && nfree) atomicAdd(nfree_out, nfree);
     }
   }
 }
 
 // A FREE-class voxel (box_class): v_new = 1, so V' = (V W + 1)/(W + 1) (= 1 exactly when V = 1, see
-// fuse_voxel) and W' = min(W + 1, W_max), each rounded once -- the oracle's update without its
+// fuse_voxel) and W' = min(W + 1, W_max), each rounded once -- the definition's update without its
 // projection, whose every possible outcome was proven to be "updated with v_new = 1".
 template <typename T>
 __device__ __forceinline__ bool fuse_free(const Geom& g, T Vs, T Ws, T* __restrict__ V, T* __restrict__ W, uint32_t o) {
@@ -398,7 +404,12 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
                                                         const double4* __restrict__ tab, const uint32_t* __restrict__ list,
                                                         const uint32_t* __restrict__ count, T* __restrict__ V,
                                                         T* __restrict__ W, uint32_t* __restrict__ dirty,
-                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount) {
+                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount,
+                                                        unsigned long long* __restrict__ nupd) {
+  __shared__ unsigned sUpd;
+  if (threadIdx.x == 0) sUpd = 0u;
+  __syncthreads();
+  unsigned upd = 0u;  // voxels this thread updated (work counter, pft_integrate_stats)
   const int n0 = 4 * g.nbx, n1 = 4 * g.nby;
   const uint32_t n = *count;
   const uint32_t w = threadIdx.x & 63;
@@ -415,9 +426,11 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
     if (i < g.nx && j < g.ny && k < g.nz) {
       const uint32_t o = b * 64u + w;
       const T Vs = V[o], Ws = W[o];  // issued first: independent of the projection chain
+      bool updated = true;
       changed = free_class ? fuse_free<T>(g, Vs, Ws, V, W, o)
                            : fuse_voxel<T>(g, K, depth, ld_axis(tab + i), ld_axis(tab + n0 + j),
-                                           ld_axis(tab + n0 + n1 + k), Vs, Ws, V, W, o);
+                                           ld_axis(tab + n0 + n1 + k), Vs, Ws, V, W, o, updated);
+      upd += updated ? 1u : 0u;
     }
     // cell-bricks whose records read this voxel: (b - d) for d in {0,1}^3, the -1 neighbours
     // only from the brick's low faces
@@ -431,7 +444,13 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
     nbm = __reduce_or_sync(0xffffffffu, nbm);
     if (nbm) mark_dirty_cells_warp(g, bx, by, bz, nbm, dirty, dlist, dcount);  // warp-uniform
   }
+  upd = __reduce_add_sync(0xffffffffu, upd);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(&sUpd, upd);
+  __syncthreads();
+  if (threadIdx.x == 0 && sUpd) atomicAdd(nupd, (unsigned long long)sUpd);
 }
+
+__global__ void k_mark_sweep(uint32_t* flag) { *flag = 1u; }
 
 // Co-resident CTAs of `kern` at `threads` per CTA on the current device (cached per kernel and device).
 template <typename K>
@@ -473,6 +492,8 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
       PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_sweep<__half><<<grid, 256, 0, st>>>(g, K, depth, tab, (__half*)(vol->base + vol->L.v_off),
                                                       (__half*)(vol->base + vol->L.w_off), n));
     records_rebuild_all(vol, st);
+    // pft_integrate_stats: the full sweep does not maintain the counters (scratch +268 = 1)
+    k_mark_sweep<<<1, 1, 0, st>>>((uint32_t*)(vol->base + vol->L.scratch_off + 268));
     return cuda_check("integrate (full sweep)");
   }
   uint2* tiles = (uint2*)(vol->base + vol->L.tiles_off);
@@ -481,7 +502,8 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   uint32_t* dcount = (uint32_t*)(vol->base + vol->L.scratch_off + 128);
   uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
   uint32_t* dlist = (uint32_t*)(vol->base + vol->L.dlist_off);
-  cudaMemsetAsync(count, 0, 192, st);  // active, dirty and super-brick counts (scratch +64..+255)
+  unsigned long long* nupd = (unsigned long long*)(vol->base + vol->L.scratch_off + 256);
+  cudaMemsetAsync(count, 0, 256, st);  // kept, dirty, super-brick counts, updated voxels, free bricks, sweep flag (+64..+319)
   cudaMemsetAsync(tiles + P.off(4), 0, sizeof(uint2) * (size_t)(P.total - P.off(4)), st);  // levels 4-5 (atomicMax targets)
   {
     const int nreg = P.nx(3) * P.ny(3);
@@ -493,16 +515,17 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   uint32_t* slist = (uint32_t*)(vol->base + vol->L.slist_off);
   uint32_t* scount = (uint32_t*)(vol->base + vol->L.scratch_off + 192);
   PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, nsz, slist, scount));
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count));
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count,
+                                                                                   (uint32_t*)(vol->base + vol->L.scratch_off + 264)));
   // grid = the resident capacity (one wave: no partial second wave of CTAs, the CTA-stride loop
   // balances the bricks)
   const int grid = vol->esize == 4 ? resident_grid(k_integrate_list<float>, 256) : resident_grid(k_integrate_list<__half>, 256);
   if (vol->esize == 4)
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (float*)(vol->base + vol->L.v_off),
-                                                  (float*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
+                                                  (float*)(vol->base + vol->L.w_off), dirty, dlist, dcount, nupd));
   else
     PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (__half*)(vol->base + vol->L.v_off),
-                                                   (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount));
+                                                   (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount, nupd));
   records_rebuild_dirty(vol, st);
   return cuda_check("integrate");
 }
@@ -519,6 +542,26 @@ pft_status pft_integrate_ex(pft_volume* vol, const uint16_t* dev_depth, const pf
   pft_status s = check_intrinsics(K);
   if (s != PFT_OK) return s;
   return integrate_impl(vol, dev_depth, K, dev_T, flags & 1, (cudaStream_t)stream);
+}
+
+pft_status pft_integrate_stats(const pft_volume* vol, int64_t out[4], void* stream) {
+  if (!vol || !out) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  uint32_t w[80];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(w, vol->base + vol->L.scratch_off, sizeof w, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return cuda_check("integrate_stats");
+  if (w[268 / 4]) {
+    for (int i = 0; i < 4; ++i) out[i] = -1;
+    return PFT_OK;
+  }
+  unsigned long long upd;
+  memcpy(&upd, (const char*)w + 256, 8);
+  out[0] = w[64 / 4];
+  out[1] = w[264 / 4];
+  out[2] = (int64_t)upd;
+  out[3] = w[128 / 4];
+  return PFT_OK;
 }
 
 pft_status pft_integrate(pft_volume* vol, const uint16_t* dev_depth, const pft_intrinsics* K, const double* dev_T,

@@ -77,6 +77,8 @@ struct pft_volume {
   char* xown;
   size_t xbytes, xcnt_off;
   int32_t xmax_particles;
+  int partition;      // PFT_PARTITION_PARTICLES (default) | PFT_PARTITION_POINTS (F2b)
+  unsigned long long preflight_round;  // pft_comm_p2p_preflight calls so far
   // one-GPU emulation: the exchange counters are zeroed when the workspace changes
   const char* xws_last;
   size_t xws_total, xws_region, xws_xcnt;  // workspace + layout the counters were zeroed for
@@ -135,6 +137,8 @@ struct TrackLayout {
   size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
   size_t work_off;     // persistent path: per-iteration work counters
   size_t topk_off;     // F3 top-k: per-block candidate lists and the merged result
+  size_t cacc_off;     // F2b point shards: the centre's partial (S, n) as 2 uint64 (all-reduced)
+  int points_part;     // F2b: particles unsharded (kloc = K), points sharded across the ranks
   size_t total;         // bytes of the whole workspace (G regions in the fused emulation)
   size_t region;        // bytes of one rank's region
   size_t xch_off;       // fused emulation: the rank's exchange buffer inside its region
@@ -151,6 +155,8 @@ namespace pft {
 pft_status fail(pft_status s, const char* fmt, ...);
 // cudaGetLastError() after a launch sequence -> PFT_OK or PFT_ERR_CUDA with the message.
 pft_status cuda_check(const char* what);
+// F2 peer exchange pre-flight (track.cu): one exchange of tokens with every attached peer.
+pft_status p2p_preflight(pft_volume* vol, int timeout_ms, int32_t* ok_out, cudaStream_t st);
 // Launch instrumentation (abi.cu): call prof_begin before and prof_end after each launch.
 void prof_begin(int cls, cudaStream_t st);
 void prof_end(int cls, cudaStream_t st, const char* what);

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "pft_internal.cuh"
 
@@ -513,6 +514,7 @@ struct EvalArgs {
   const unsigned long long* mask;  // in-band bits
   Geom g;
   Points pts;
+  int pbeg, pend;            // point slots [pbeg, pend) of this launch (F2b point shards; else [0, npad))
   int mode;                  // 0: template particles, 1: explicit poses
   const float* pst;          // mode 0: full K x 6 template
   int k_begin, k_count;      // particle range of this launch (absolute template rows / pose rows)
@@ -569,8 +571,8 @@ __global__ __launch_bounds__(kThreads, PFT_MINB) void k_particle_eval(EvalArgs a
   double pm = 0.0;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int i = (blockIdx.x * PPT + p) * kThreads + tid;
-    if (i < a.pts.npad) {
+    const int i = a.pbeg + (blockIdx.x * PPT + p) * kThreads + tid;
+    if (i < a.pend) {
       px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i];
     } else {
       px[p] = py[p] = pz[p] = 0.0;
@@ -721,7 +723,11 @@ struct CentreArgs {
   double beta, rho;
   StopRule sr;
   double* trace;
+  int pbeg, pend;                   // point slots of this launch
+  unsigned long long* cacc;         // F2b: non-null = partial mode, accumulate (S, n) here only
 };
+
+__device__ __noinline__ void centre_finish(const CentreArgs& a, unsigned long long S, unsigned ncn);
 
 template <typename T>
 __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
@@ -740,9 +746,9 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
     double px[kCentrePPT], py[kCentrePPT], pz[kCentrePPT], pm = 0.0;
 #pragma unroll
     for (int p = 0; p < kCentrePPT; ++p) {
-      const int i = (blockIdx.x * kCentrePPT + p) * kThreads + tid;
+      const int i = a.pbeg + (blockIdx.x * kCentrePPT + p) * kThreads + tid;
       px[p] = py[p] = pz[p] = 0.0;
-      if (i < a.pts.npad) { px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i]; }
+      if (i < a.pend) { px[p] = a.pts.x[i]; py[p] = a.pts.y[i]; pz[p] = a.pts.z[i]; }
       pm = fmax(pm, fmax(fabs(px[p]), fmax(fabs(py[p]), fabs(pz[p]))));
     }
     const double pmax = block_max(pm, sRed);
@@ -765,10 +771,16 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
     unsigned n;
     warp_total64(sum, cnt, S, n);
     if ((tid & 31) == 0 && n) {
-      atomicAdd(&st->Sc_acc, S);
-      atomicAdd(&st->nc_acc, n);
+      if (a.cacc) {  // F2b partial: the rank's slice only; summed across ranks, then k_centre_finish
+        atomicAdd(a.cacc, S);
+        atomicAdd(a.cacc + 1, (unsigned long long)n);
+      } else {
+        atomicAdd(&st->Sc_acc, S);
+        atomicAdd(&st->nc_acc, n);
+      }
     }
   }
+  if (a.cacc) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) sLast = atomicAdd(&st->ticket_ctr, 1u) == gridDim.x - 1;
@@ -776,12 +788,20 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
   if (!sLast || tid != 0) return;
   __threadfence();
   volatile TrackState* vs = st;
-  const int N = vs->Nvalid[a.set];
   const unsigned long long S = vs->Sc_acc;
   const unsigned ncn = vs->nc_acc;
   st->Sc_acc = 0ull;
   st->nc_acc = 0u;
   st->ticket_ctr = 0u;
+  centre_finish(a, S, ncn);
+}
+
+// The centre's E(P) from its summed (S, n) (one thread): baseline (mode 0), or after the update
+// (mode 1) the F3 guard, the s-law, stalls / stop rule and the trace row.
+__device__ __noinline__ void centre_finish(const CentreArgs& a, unsigned long long S, unsigned ncn) {
+  TrackState* st = a.st;
+  volatile TrackState* vs = st;
+  const int N = vs->Nvalid[a.set];
   if (a.mode == 0) {
     st->Ec = fitness_c(S, ncn, a.rho, N);
     st->nc = ncn;
@@ -817,6 +837,19 @@ __global__ __launch_bounds__(kThreads) void k_centre(CentreArgs a) {
     const int flags = (nA == 0 ? 1 : 0) | (Ebase == 1.0 ? 2 : 0) | (N == 0 ? 4 : 0) | (rejected ? 8 : 0) | (stop ? 16 : 0);
     write_trace(a.trace + (size_t)a.it * PFT_TRACE_DOUBLES, Ebase, nA, om, v, P, Ec, om1, v1, flags, nc, N, a.Ki, a.code);
   }
+}
+
+// F2b: the centre's finalisation after its per-rank partial sums were added across ranks
+// (cacc = (S, n) as uint64); re-zeroes cacc for the next centre.
+__global__ void k_centre_finish(CentreArgs a) {
+  if (a.st->stopped) {
+    if (a.mode == 1 && a.trace) write_not_run(a.trace + (size_t)a.it * PFT_TRACE_DOUBLES);
+    return;
+  }
+  const unsigned long long S = a.cacc[0], n = a.cacc[1];
+  a.cacc[0] = 0ull;
+  a.cacc[1] = 0ull;
+  centre_finish(a, S, (unsigned)n);
 }
 
 // a7: E_k, advantage set A = {k < K_i : E_k < E_base}, (weighted) mean delta over A
@@ -978,6 +1011,14 @@ struct PArgs {
   char* xbuf[kMaxFusedRanks];
   size_t o_xcnt;
   size_t xhalf;  // records per exchange half: fixed per buffer (a peer may still read the previous call's half)
+  unsigned long long watchdog_ns;  // grid-barrier / exchange wait before a trap (PFT_WATCHDOG_MS)
+};
+
+// Peer-exchange buffers of one rank's job (pre-flight).
+struct PArgsX {
+  int G, rank;
+  char* xbuf[kMaxFusedRanks];
+  size_t pre_off;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -997,8 +1038,10 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // and polls with acquire loads (LDG.STRONG.GPU + CCTL.IVALL, so data other CTAs wrote before the
 // barrier is read fresh after it) until all nb CTAs of this round arrived: 1.3 us vs 2.2 us for
 // a sense-reversing barrier at 296 CTAs (tools/microbench/barrier.cu).
-// Watchdog: a CTA that waits more than 5 s traps (a launch error instead of a hung GPU).
-__device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long& target, int nb) {
+// Watchdog: a CTA that waits longer than watchdog_ns (PFT_WATCHDOG_MS, default 5 s) traps (a launch
+// error instead of a hung GPU).
+__device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long& target, int nb,
+                                             unsigned long long watchdog_ns) {
   __syncthreads();
   target += (unsigned long long)nb;
   if (threadIdx.x == 0) {
@@ -1010,7 +1053,7 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
       __nanosleep(32);
       const unsigned long long now = global_ns();
       if (t0 == 0ull) t0 = now;
-      else if (now - t0 > 5000000000ull) {
+      else if (now - t0 > watchdog_ns) {
         printf("pft: grid barrier timeout (CTA %d, target %llu)\n", blockIdx.x, target);
         __trap();
       }
@@ -1084,7 +1127,6 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   __shared__ unsigned long long sS[kThreads / 32];
   __shared__ unsigned sNw[kThreads / 32];
   __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
-  __shared__ int sWFlag[kThreads / 32][kItemParticles];
   __shared__ int sTopSel[kTopkMax];
   // per-lane partials of the item's particles: (fix | cnt << 32), rows padded against bank conflicts
   unsigned long long (*sPart)[kItemParticles][33] =
@@ -1168,7 +1210,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     sState[0] = a.omega0; sState[1] = a.v0; sState[2] = 1.0;
     sStalls = 0; sStop = 0; sSet = -1; sKlast = 0; sNc = 0u; sNA = 0;
   }
-  grid_barrier(st, gen, nb);
+  grid_barrier(st, gen, nb, a.watchdog_ns);
 #define PFT_TMARK(slot)                                        \
   if (timing && tid == 0) {                                    \
     const unsigned long long now_ = global_ns();               \
@@ -1196,7 +1238,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       block_total(sum, cnt, sS, sNw, S, n);
       // half 0 of the centre partials: P5 of the previous iteration may still be reading half 1
       if (tid == 0) { cpart[2 * lb] = S; cpart[2 * lb + 1] = n; }
-      grid_barrier(st, gen, nb);
+      grid_barrier(st, gen, nb, a.watchdog_ns);
       unsigned long long S2, n2;
       sum_partials(cpart, nb, sS, sNw, S2, n2);
       if (tid == 0) {
@@ -1215,7 +1257,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
 #pragma unroll
       for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
     }
-    grid_barrier(st, gen, nb);
+    grid_barrier(st, gen, nb, a.watchdog_ns);
     PFT_TMARK(1);
     // F2: this rank's shard of the K_i particles, local rows [0, Ks) = global rows [kb, kb + Ks)
     const int Ks = max(0, min(Ki, kb + kloc) - kb);
@@ -1263,19 +1305,19 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
           px[p] = py[p] = pz[p] = 0.0;
           if (i < pts.npad) { px[p] = __ldcg(pts.x + i); py[p] = __ldcg(pts.y + i); pz[p] = __ldcg(pts.z + i); }
         }
-        // stage the item's poses in this warp's shared slot (6 x 16 B per pose, 3 per lane)
+        // stage the item's poses in this warp's shared slot (6 x 16 B per pose, 3 per lane); the
+        // item's pose flags as two warp-uniform bit masks (no per-particle shared-memory load)
         double2* wp = sWPose[tid >> 5];
-        int* wf = sWFlag[tid >> 5];
         __syncwarp();
         for (int q = lane; q < (k1 - k0) * 6; q += 32) wp[q] = __ldcg((const double2*)(ptab + 12 * (size_t)(kb + k0)) + q);
-        if (lane < k1 - k0) wf[lane] = __ldcg(pflag + kb + k0 + lane);
+        const int myflag = lane < k1 - k0 ? __ldcg(pflag + kb + k0 + lane) : 0;
+        const unsigned fvalid = __ballot_sync(0xffffffffu, myflag != 0), ffast = __ballot_sync(0xffffffffu, myflag == 2);
         __syncwarp();
         unsigned long long (*part)[33] = sPart[tid >> 5];
         for (int k = k0; k < k1; ++k) {
-          const int flag = wf[k - k0];
           unsigned sum = 0u;
           unsigned cnt = 0u;
-          if (flag != 0) {  // warp-uniform
+          if ((fvalid >> (k - k0)) & 1u) {  // warp-uniform
             double m[12];
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
@@ -1283,7 +1325,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
               m[2 * q] = v.x;
               m[2 * q + 1] = v.y;
             }
-            if (flag == 2) eval_points<T, true, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
+            if ((ffast >> (k - k0)) & 1u) eval_points<T, true, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
             else eval_points<T, false, kItemTiles>((const T*)a.R, a.mask, a.g, m, px, py, pz, sum, cnt);
           }
           part[k - k0][lane] = (unsigned long long)sum | ((unsigned long long)cnt << 32);
@@ -1310,7 +1352,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       __syncthreads();
       if (tid == 0) a.tdone[lb] = global_ns();
     }
-    grid_barrier(st, gen, nb);
+    grid_barrier(st, gen, nb, a.watchdog_ns);
     if (timing && tid == 0 && lb == 0) {
       unsigned long long lo = ~0ull, hi = 0ull;
       for (int b = 0; b < (int)nb; ++b) {
@@ -1336,7 +1378,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         acc[j].n = 0u;
       }
       __threadfence_system();
-      grid_barrier(st, gen, nb);
+      grid_barrier(st, gen, nb, a.watchdog_ns);
       if (lb == 0 && tid < G) {
         __threadfence_system();
         atomicAdd_system((unsigned long long*)(sXbuf[tid] + a.o_xcnt) + grp, 1ull);
@@ -1348,7 +1390,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         for (int q = 0; q < G; ++q)
           while (ld_acquire_sys(cnt + q) < target) {
             __nanosleep(32);
-            if (global_ns() - t0 > 5000000000ull) {
+            if (global_ns() - t0 > a.watchdog_ns) {
               printf("pft: exchange timeout (rank %d CTA %d source %d round %llu)\n", grp, lb, q, target);
               __trap();
             }
@@ -1397,14 +1439,14 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         __syncthreads();
       }
     }
-    grid_barrier(st, gen, nb);
+    grid_barrier(st, gen, nb, a.watchdog_ns);
     PFT_TMARK(3);
     // ---- P4: combine partials (fixed tree, identical in every CTA) -> P; centre slice
     if (a.rule == 2) {
       // F3 top-k: CTA 0 merges the blocks' sorted candidates and sums the selected deltas
       if (lb == 0)
         topk_finish(ckey, cidx, nblk, a.topk, a.pst, sState[0], sState[1], tkout, tkey, tidx, sTopSel);
-      grid_barrier(st, gen, nb);
+      grid_barrier(st, gen, nb, a.watchdog_ns);
       if (tid < 8) red[tid][0] = __ldcg(tkout + tid);
       if (tid == 8) red[8][0] = __ldcg(tkout + 7);  // weight sum = number selected
       __syncthreads();
@@ -1442,7 +1484,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       // half 1 of the centre partials (read in P5 below; the next baseline B writes half 0)
       unsigned long long* cp1 = cpart + 2 * (size_t)nb;
       if (tid == 0) { cp1[2 * lb] = S; cp1[2 * lb + 1] = n; }
-      grid_barrier(st, gen, nb);  // sNA is identical in every CTA: uniform barrier
+      grid_barrier(st, gen, nb, a.watchdog_ns);  // sNA is identical in every CTA: uniform barrier
     }
     PFT_TMARK(4);
     // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
@@ -1549,12 +1591,15 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
     }
     L->sched_set[j] = found;
   }
-  L->kloc = (nparticles + nranks - 1) / nranks;
+  // F2b point shards (virtual or NCCL, G > 1): every rank holds all K records
+  L->points_part = vol && vol->partition == PFT_PARTITION_POINTS && nranks > 1 && !vol->virtual_fused && !vol->p2p;
+  L->kloc = L->points_part ? nparticles : (nparticles + nranks - 1) / nranks;
   L->kfull = L->kloc * nranks;
   L->nblk_upd = (nparticles + 255) / 256;
   L->acc_local_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kloc, 256);
-  if (nranks > 1) { L->acc_full_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kfull, 256); }
-  else L->acc_full_off = L->acc_local_off;
+  if (nranks > 1 && !L->points_part) { L->acc_full_off = off; off = align_up(off + sizeof(PartRec) * (size_t)L->kfull, 256); }
+  else L->acc_full_off = L->acc_local_off;  // (point shards: the records are all-reduced in place)
+  L->cacc_off = off; off = align_up(off + 2 * sizeof(unsigned long long), 256);
   L->part_off = off; off = align_up(off + kUpdW * sizeof(double) * (size_t)L->nblk_upd, 256);
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
   L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
@@ -1575,6 +1620,14 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
 }
 
 pft_status comm_allgather(pft_volume* vol, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st);
+pft_status comm_allreduce_u64(pft_volume* vol, void* buf, size_t count, cudaStream_t st);
+
+// F2b: point slots of rank q of G -- whole 8x4 tiles (32 slots), contiguous.
+static void point_slice(int npad, int G, int q, int& b, int& e) {
+  const int tiles = npad / 32, per = (tiles + G - 1) / G;
+  b = min(npad, q * per * 32);
+  e = min(npad, (q + 1) * per * 32);
+}
 
 struct Launch {
   pft_volume* vol;
@@ -1614,34 +1667,100 @@ static void launch_prologue(const Launch& c, const uint16_t* depth, const pft_in
 }
 
 template <typename T>
-static void launch_centre(const Launch& c, int mode, int set, int it, int Ki, const pft_track_params* prm,
-                          double* trace) {
+static pft_status launch_centre(const Launch& c, int mode, int set, int it, int Ki, const pft_track_params* prm,
+                                double* trace) {
   const PSet s = c.set(set);
   CentreArgs ca{c.vol->base + c.vol->L.v_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g,
                 s.pts(), c.state(), mode, set, it, Ki, s.sx + 1000 * s.sy, prm->guard, prm->beta,
-                prm->min_inband_frac, StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit}, trace};
-  int grid = (s.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
-  PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
+                prm->min_inband_frac, StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit}, trace,
+                0, s.npad, nullptr};
+  if (!c.L.points_part) {
+    const int grid = (s.npad + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
+    PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
+    return PFT_OK;
+  }
+  // F2b: this rank's slice (virtual shards: every slice in turn) into the partial sums, their sum
+  // across the ranks (NCCL all-reduce; the virtual slices already share one accumulator), finish
+  ca.cacc = (unsigned long long*)(c.ws + c.L.cacc_off);
+  const int G = c.vol->nranks;
+  for (int q = 0; q < G; ++q) {
+    if (c.vol->virtual_ranks <= 1 && q != c.vol->rank) continue;
+    point_slice(s.npad, G, q, ca.pbeg, ca.pend);
+    const int grid = (ca.pend - ca.pbeg + kThreads * kCentrePPT - 1) / (kThreads * kCentrePPT);
+    if (grid > 0) PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre<T><<<grid, kThreads, 0, c.st>>>(ca));
+  }
+  if (c.vol->virtual_ranks <= 1) {
+    const pft_status r = comm_allreduce_u64(c.vol, ca.cacc, 2, c.st);
+    if (r != PFT_OK) return r;
+  }
+  PFT_LAUNCH(PFT_PROF_CENTRE, c.st, k_centre_finish<<<1, 1, 0, c.st>>>(ca));
+  return PFT_OK;
 }
 
 template <typename T>
 static void launch_eval(const Launch& c, int mode, const float* pst, int k_begin, int k_count, int conv,
-                        const double* poses, PartRec* acc, int set) {
+                        const double* poses, PartRec* acc, int set, int pbeg = 0, int pend = -1) {
   if (k_count <= 0) return;
   const PSet s = c.set(set);
+  if (pend < 0) pend = s.npad;
+  if (pend <= pbeg) return;
   EvalArgs ea{c.vol->base + c.vol->L.r_off, (const unsigned long long*)(c.vol->base + c.vol->L.m_off), c.vol->g,
-              s.pts(), mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
-  dim3 grid((s.npad + kThreads * kPPT - 1) / (kThreads * kPPT), (k_count + kPC - 1) / kPC);
+              s.pts(), pbeg, pend, mode, pst, k_begin, k_count, c.state(), conv, poses, acc};
+  dim3 grid((pend - pbeg + kThreads * kPPT - 1) / (kThreads * kPPT), (k_count + kPC - 1) / kPC);
   static const int ppt = [] {  // tuning knob for experiments: PFT_EVAL_PPT=2|4
     const char* e = getenv("PFT_EVAL_PPT");
     return e && atoi(e) == 2 ? 2 : kPPT;
   }();
   if (ppt == 2) {
-    grid.x = (s.npad + kThreads * 2 - 1) / (kThreads * 2);
+    grid.x = (pend - pbeg + kThreads * 2 - 1) / (kThreads * 2);
     PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, 2><<<grid, kThreads, 0, c.st>>>(ea));
   } else {
     PFT_LAUNCH(PFT_PROF_EVAL, c.st, k_particle_eval<T, kPPT><<<grid, kThreads, 0, c.st>>>(ea));
   }
+}
+
+// Co-resident CTAs of k_track_persistent<T> on the current device (cached per device; the carveout
+// attribute is set once per device before the occupancy query).  Shared-memory carveout: the
+// smallest that keeps 2 CTAs/SM resident, so the rest of the unified 256 KB stays L1 for the record
+// and mask gathers (measured: 1.584 vs 1.597 ms with the driver's default; PFT_CARVEOUT=<percent>
+// overrides).
+template <typename T>
+static int persistent_cap() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& cap = cache[dev & 63];
+  if (cap != 0) return cap;
+  int per_sm = 0, sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int carve = -1;
+  if (const char* e = getenv("PFT_CARVEOUT")) {
+    carve = atoi(e);
+  } else {
+    cudaFuncAttributes fa;
+    int smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (cudaFuncGetAttributes(&fa, k_track_persistent<T>) == cudaSuccess && smem_sm > 0)
+      carve = (int)((200.0 * ((double)fa.sharedSizeBytes + 1024.0) + smem_sm - 1) / smem_sm);
+  }
+  if (carve >= 0 && carve <= 100)
+    cudaFuncSetAttribute(k_track_persistent<T>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kThreads, 0);
+  cap = per_sm * sms;
+  if (cap > 148 * 8) cap = 148 * 8;
+  if (cap < 1) cap = -1;
+  return cap;
+}
+
+static unsigned long long watchdog_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = getenv("PFT_WATCHDOG_MS");
+    const long long ms = e ? atoll(e) : 5000;
+    return (unsigned long long)(ms > 0 ? ms : 5000) * 1000000ull;
+  }();
+  return ns;
 }
 
 // Persistent single-launch tracker: cooperative launch, all CTAs co-resident.  G = 1; or G rank
@@ -1651,31 +1770,8 @@ template <typename T>
 static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_intrinsics* K, const double* T_init,
                                    const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                                    int32_t* n_out, double* trace) {
-  static int cap = 0;
-  if (cap == 0) {
-    int per_sm = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // Shared-memory carveout: the smallest that keeps 2 CTAs/SM resident, so the rest of the
-    // unified 256 KB stays L1 for the record and mask gathers (measured: 1.584 vs 1.597 ms with the
-    // driver's default; PFT_CARVEOUT=<percent> overrides)
-    int carve = -1;
-    if (const char* e = getenv("PFT_CARVEOUT")) {
-      carve = atoi(e);
-    } else {
-      cudaFuncAttributes fa;
-      int smem_sm = 0;
-      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-      if (cudaFuncGetAttributes(&fa, k_track_persistent<T>) == cudaSuccess && smem_sm > 0)
-        carve = (int)((200.0 * ((double)fa.sharedSizeBytes + 1024.0) + smem_sm - 1) / smem_sm);
-    }
-    if (carve >= 0 && carve <= 100)
-      cudaFuncSetAttribute(k_track_persistent<T>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kThreads, 0);
-    cap = per_sm * sms;
-    if (cap > 148 * 8) cap = 148 * 8;
-    if (cap < 1) return fail(PFT_ERR_CUDA, "persistent tracker does not fit on the device");
-  }
+  const int cap = persistent_cap<T>();
+  if (cap < 1) return fail(PFT_ERR_CUDA, "persistent tracker does not fit on the device");
   pft_volume* vol = c.vol;
   const bool emul = vol->virtual_fused && vol->nranks > 1;
   const int G = (emul || vol->p2p) ? vol->nranks : 1;
@@ -1708,6 +1804,7 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   static const bool timing = [] { const char* e = getenv("PFT_PHASE_TIMING"); return e && e[0] == '1'; }();
   pa.tdone = (timing && !emul) ? (unsigned long long*)(c.ws + c.L.work_off + 1024 * sizeof(unsigned)) : nullptr;
   pa.topk = prm->topk;
+  pa.watchdog_ns = watchdog_ns();
   pa.ws = c.ws;
   pa.rank_stride = region;
   pa.o_state = c.L.state_off;
@@ -1779,17 +1876,35 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
     // the cooperative grid does not fit right now (G = 1): same results from the multi-launch path
   }
   const int kloc = c.L.kloc;
-  const int k_begin = r * kloc;
+  const int k_begin = c.L.points_part ? 0 : r * kloc;
   PartRec* local = (PartRec*)(c.ws + c.L.acc_local_off);
   PartRec* full = (PartRec*)(c.ws + c.L.acc_full_off);
   launch_prologue(c, depth, K, T_init, prm->omega0_deg, prm->v0_cm);
+  if (c.L.points_part) cudaMemsetAsync(c.ws + c.L.cacc_off, 0, 2 * sizeof(unsigned long long), c.st);
   int prev_set = -1;
   for (int it = 0; it < prm->iters; ++it) {
     const int j = it % c.L.nsched;
     const int Ki = c.L.sched_K[j], set = c.L.sched_set[j];
-    if (set != prev_set) launch_centre<T>(c, 0, set, it, Ki, prm, trace);  // baseline on the new set (L11)
+    if (set != prev_set) {  // baseline on the new set (L11)
+      const pft_status s = launch_centre<T>(c, 0, set, it, Ki, prm, trace);
+      if (s != PFT_OK) return s;
+    }
     prev_set = set;
-    if (c.vol->virtual_ranks > 1) {
+    if (c.L.points_part) {
+      // F2b: all K_i particles on this rank's point slice (virtual: every slice in turn into the same
+      // accumulators), the per-particle sums added across the ranks in place (exact integers)
+      const int npad = c.set(set).npad;
+      for (int q = 0; q < G; ++q) {
+        if (c.vol->virtual_ranks <= 1 && q != r) continue;
+        int pb, pe;
+        point_slice(npad, G, q, pb, pe);
+        launch_eval<T>(c, 0, pst, 0, Ki, prm->delta_conv, nullptr, local, set, pb, pe);
+      }
+      if (c.vol->virtual_ranks <= 1) {
+        const pft_status s = comm_allreduce_u64(c.vol, local, 2 * (size_t)Ki, c.st);
+        if (s != PFT_OK) return s;
+      }
+    } else if (c.vol->virtual_ranks > 1) {
       // virtual shards: rank q's evaluation, then its all-gather slot filled by a device copy
       for (int q = 0; q < G; ++q) {
         const int kb = q * kloc, kc = max(0, min(Ki, kb + kloc) - kb);
@@ -1811,7 +1926,8 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
                c.state(), full, local, Ki, k_begin, kloc, pst, prm->delta_conv, prm->update_rule, set,
                prm->min_inband_frac, E, n_out, (double*)(c.ws + c.L.part_off)};
     PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_update<<<(Ki + 255) / 256, 256, 0, c.st>>>(ua));
-    launch_centre<T>(c, 1, set, it, Ki, prm, trace);
+    const pft_status s = launch_centre<T>(c, 1, set, it, Ki, prm, trace);
+    if (s != PFT_OK) return s;
   }
   PFT_LAUNCH(PFT_PROF_UPDATE, c.st, k_track_finalize<<<(Kp + 255) / 256, 256, 0, c.st>>>(c.state(), Kp, E, n_out, T_out));
   return cuda_check("track");
@@ -1846,11 +1962,73 @@ static pft_status check_params(const pft_track_params* p) {
   return PFT_OK;
 }
 
+// F2 pre-flight: one block; thread q < G stores this rank's token into slot [rank] of rank q's
+// preflight array (system-scope release store over NVLink), then thread 0 polls its own array until
+// every slot holds the round's token of its writer (acquire loads), for at most timeout_ns.
+__global__ void k_p2p_preflight(PArgsX x, unsigned long long round, unsigned long long timeout_ns, int* ok) {
+  const int q = threadIdx.x;
+  if (q < x.G) {
+    unsigned long long* dst = (unsigned long long*)(x.xbuf[q] + x.pre_off) + x.rank;
+    const unsigned long long tok = (round << 8) | (unsigned long long)(x.rank + 1);
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(tok) : "memory");
+  }
+  __syncthreads();
+  if (q != 0) return;
+  const unsigned long long* mine = (const unsigned long long*)(x.xbuf[x.rank] + x.pre_off);
+  const unsigned long long t0 = global_ns();
+  int good = 1;
+  for (int r = 0; r < x.G && good; ++r) {
+    const unsigned long long want = (round << 8) | (unsigned long long)(r + 1);
+    for (;;) {
+      const unsigned long long v = ld_acquire_sys(mine + r);
+      if (v == want) break;
+      if (global_ns() - t0 > timeout_ns) { good = 0; break; }
+      __nanosleep(64);
+    }
+  }
+  *ok = good;
+}
+
+pft_status p2p_preflight(pft_volume* vol, int timeout_ms, int32_t* ok_out, cudaStream_t st) {
+  PArgsX x;
+  x.G = vol->nranks;
+  x.rank = vol->rank;
+  for (int q = 0; q < kMaxFusedRanks; ++q) x.xbuf[q] = q < vol->nranks ? vol->xbuf[q] : nullptr;
+  x.pre_off = vol->xcnt_off + (kMaxFusedRanks + 1) * sizeof(unsigned long long);
+  int* d_ok = nullptr;
+  int h_ok = 0;
+  if (cudaMallocAsync((void**)&d_ok, sizeof(int), st) != cudaSuccess) return cuda_check("preflight (alloc)");
+  const unsigned long long round = ++vol->preflight_round;
+  k_p2p_preflight<<<1, 32, 0, st>>>(x, round, (unsigned long long)timeout_ms * 1000000ull, d_ok);
+  cudaMemcpyAsync(&h_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_ok, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("preflight");
+  *ok_out = h_ok;
+  return cuda_check("preflight");
+}
+
+// out = A * B for rigid 3x4 row-major [R|t] poses: (R_A R_B, R_A t_B + t_A).
+__global__ void k_pose_compose(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ out) {
+  const int i = threadIdx.x;  // threads 0..11: element (r, c)
+  const int r = (i >> 2) % 3, c = i & 3;
+  double v = A[4 * r + 0] * B[c] + A[4 * r + 1] * B[4 + c] + A[4 * r + 2] * B[8 + c];
+  if (c == 3) v += A[4 * r + 3];
+  __syncthreads();
+  if (i < 12) out[i] = v;  // (out may alias A or B: every read happens before the barrier)
+}
+
 }  // namespace pft
 
 using namespace pft;
 
 extern "C" {
+
+pft_status pft_pose_compose(const double* dev_A, const double* dev_B, double* dev_out, void* stream) {
+  if (!dev_A || !dev_B || !dev_out) return fail(PFT_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  PFT_LAUNCH(PFT_PROF_OTHER, st, k_pose_compose<<<1, 32, 0, st>>>(dev_A, dev_B, dev_out));
+  return cuda_check("pose_compose");
+}
 
 pft_status pft_track_workspace_bytes(const pft_volume* vol, const pft_intrinsics* K, int32_t nparticles,
                                      const pft_track_params* prm, size_t* bytes_out) {

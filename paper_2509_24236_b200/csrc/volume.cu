@@ -295,6 +295,7 @@ pft_status pft_volume_create(const pft_volume_desc* desc, void* dev_storage, siz
   cudaGetDevice(&v->device);
   v->nccl_comm = nullptr; v->nranks = 1; v->rank = 0; v->virtual_ranks = 0; v->virtual_fused = 0;
   v->p2p = 0; v->xown = nullptr; v->xbytes = 0; v->xcnt_off = 0; v->xmax_particles = 0;
+  v->partition = PFT_PARTITION_PARTICLES; v->preflight_round = 0;
   for (int q = 0; q < PFT_MAX_FUSED_RANKS; ++q) v->xbuf[q] = nullptr;
   v->xws_last = nullptr; v->xws_total = v->xws_region = v->xws_xcnt = 0;
   *out = v;

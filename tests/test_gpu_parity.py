@@ -325,7 +325,11 @@ def test_integrate_room_bit_exact(pft, storage):
         depth = render_depth(scene, intr, Tf, Stream(4, 4_000_000 + f))
         vol.integrate(T(depth), intr, T(Tf))
         vol_full.integrate(T(depth), intr, T(Tf), full_sweep=True)
-        ov.integrate(depth, intr, Tf)
+        n_ora = ov.integrate(depth, intr, Tf)
+        st = vol.integrate_stats()  # the culled path's work counters: updated voxels = the definition's
+        assert st["updated_voxels"] == n_ora, (st, n_ora)
+        assert 0 < st["free_bricks"] <= st["kept_bricks"] and st["dirty_cell_bricks"] > 0
+        assert vol_full.integrate_stats()["updated_voxels"] == -1
     V, W = [x.cpu().numpy() for x in vol.download()]
     Vf, Wf = [x.cpu().numpy() for x in vol_full.download()]
     assert np.array_equal(storage_bits(V), storage_bits(Vf)) and np.array_equal(storage_bits(W), storage_bits(Wf))
@@ -683,3 +687,57 @@ def test_debug_build_bounds_checked(tmp_path):
             outs[name] = np.load(f)
         for k in ("T", "E", "n", "trace"):
             assert np.array_equal(outs["prod"][k], outs["debug"][k]), (cfg, k)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_point_shards_bit_identical(pft, G):
+    """F2b point-sharded partition (include/pft.h pft_comm_set_partition), emulated on one GPU with G
+    virtual ranks: every rank evaluates all K_i particles on its contiguous slice of point tiles and
+    the fixed-point sums -- per particle and of the centre -- are added across the slices (what the
+    NCCL all-reduce does across GPUs).  Equals the 1-rank run bit for bit (config S, top-k, a
+    scheduled ragged-K weighted/guarded run) and the oracle."""
+    import dataclasses
+    cases = []
+    c = config_single(seed=1)
+    cases.append(("single", c, c["pst"], c["params"]))
+    c = config_single(seed=2)
+    cases.append(("single_topk", c, c["pst"], dataclasses.replace(c["params"], update_rule=2, topk=32, iters=4)))
+    c = config_tiny(seed=2)
+    cases.append(("tiny_sched", c, make_pst(2, 61),
+                  dataclasses.replace(TrackParams(iters=7, stride=1, guard=1, update_rule=1), **SCHED_TINY)))
+    for name, c, pst, params in cases:
+        ref = gpu_volume(pft, c["desc"], c["V"], c["W"])
+        a = run_track(pft, ref, c["depth"], c["intr"], c["T_init"], pst, params)
+        ref.close()
+        vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+        vol.comm_init_virtual(G)
+        vol.set_partition(True)
+        b = run_track(pft, vol, c["depth"], c["intr"], c["T_init"], pst, params)
+        for k in ("T", "E", "n", "trace"):
+            assert np.array_equal(a[k], b[k]), (name, G, k)
+        _assert_vs_oracle(b, c, pst, params, f"point shards G={G} {name}", key="pts " + name)
+        vol.close()
+
+
+def test_point_partition_rejected_with_peer_exchange(pft):
+    c = config_tiny(seed=1)
+    vol = gpu_volume(pft, c["desc"], c["V"], c["W"])
+    vol.comm_init_virtual(4, fused=True)
+    with pytest.raises(pft.PftError, match="UNSUPPORTED"):
+        vol.set_partition(True)
+    vol.close()
+
+
+def test_pose_compose(pft):
+    """pft_pose_compose (device-side chaining of the sequence driver's T_init = P_{t-1} rel_t) against
+    the rigid-transform product."""
+    from synth.scene import compose
+    st = Stream(21, 21)
+    for _ in range(5):
+        A = perturb(np.eye(3, 4), st.symmetric(3), st.symmetric(3), 60.0, 200.0)
+        B = perturb(np.eye(3, 4), st.symmetric(3), st.symmetric(3), 60.0, 200.0)
+        out = pft.pose_compose(T(A), T(B)).cpu().numpy()
+        np.testing.assert_allclose(out, compose(A, B), atol=1e-14)
+        a_dev = T(A)
+        pft.pose_compose(a_dev, T(B), out=a_dev)  # in place
+        np.testing.assert_allclose(a_dev.cpu().numpy(), compose(A, B), atol=1e-14)

@@ -237,3 +237,139 @@ def test_p2p_ipc_attach_two_processes():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == {0: (True, 2, 0, 1), 1: (True, 2, 1, 1)}, res
+
+
+def _preflight_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import ctypes as C
+    import paper_2509_24236_b200 as pft
+    from paper_2509_24236_b200 import api
+    from synth.configs import config_tiny
+    torch.cuda.set_device(0)
+    vol = pft.Volume(config_tiny(seed=1)["desc"], torch.device("cuda", 0))
+    L = pft.lib()
+    h = (C.c_uint8 * api.IPC_HANDLE_BYTES)()
+    assert L.pft_comm_p2p_init(vol.handle, world, rank, 64, h) == 0
+    handles = api.gather_handles(bytes(h), None)
+    raw = (C.c_uint8 * (api.IPC_HANDLE_BYTES * world))(*handles)
+    assert L.pft_comm_p2p_attach(vol.handle, raw) == 0
+    dist.barrier()
+    res = None
+    if rank == 0:
+        # rank 1 never writes its token: the pre-flight must time out and report failure (no trap,
+        # no hang) -- rank 0's kernel waits on memory only, never on another kernel
+        okp = C.c_int32(7)
+        st = L.pft_comm_p2p_preflight(vol.handle, 200, C.byref(okp), None)
+        res = (st, okp.value, int(torch.cuda.is_available()))
+        # the context is still usable afterwards
+        vol.reset()
+        torch.cuda.synchronize()
+    dist.barrier()
+    assert L.pft_comm_p2p_detach(vol.handle) == 0
+    q.put((rank, res))
+    vol.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_p2p_preflight_times_out_without_trapping():
+    """The F2 pre-flight (include/pft.h pft_comm_p2p_preflight) on real CUDA IPC between two
+    processes: with the peer silent, it returns ok = 0 within its timeout instead of trapping, and
+    the CUDA context stays usable (the caller then falls back to NCCL, api.Volume.comm_init_p2p)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_preflight_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == (0, 0, 1), res
+
+
+def _points_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from synth.configs import TrackParams, config_tiny, make_pst
+    c = config_tiny(seed=2)
+    pst = make_pst(2, 37)
+    params = TrackParams(iters=3, stride=2)
+    vol = oracle.OracleVolume(c["desc"], c["V"], c["W"])
+    pts = oracle.backproject(c["depth"], c["intr"], params.stride)
+    N = len(pts)
+    per = -(-N // world)
+    mine = pts[rank * per:(rank + 1) * per]  # this rank's slice of the points (F2b)
+
+    def fit(T):
+        """(S, n) of this rank's slice, summed across the ranks (the all-reduce), -> E, n."""
+        E, n, _ = vol.fitness(mine, T) if len(mine) else (1.0, 0, 1.0)
+        S = E * n if n > 0 else 0.0
+        t = torch.tensor([S, float(n)], dtype=torch.float64)
+        dist.all_reduce(t)
+        S, n = float(t[0]), int(t[1])
+        return (S / n if n > 0 else 1.0), n
+
+    P = np.array(c["T_init"], dtype=np.float64)
+    omega, v = params.omega0_deg, params.v0_cm
+    Ec, _ = fit(P)
+    K = len(pst)
+    trace = []
+    for it in range(params.iters):
+        E, n = np.ones(K), np.zeros(K, np.int32)
+        qs, us = np.zeros((K, 4)), np.zeros((K, 3))
+        for k in range(K):
+            dR, qs[k], us[k] = oracle.delta(pst[k], omega, v)
+            E[k], n[k] = fit(oracle.apply_delta(dR, us[k], P, params.delta_conv))
+        Ebase = Ec
+        Q, U, nA = np.zeros(4), np.zeros(3), 0
+        for k in range(K):
+            if E[k] < Ebase:
+                Q, U, nA = Q + qs[k], U + us[k], nA + 1
+        if nA > 0:
+            qn = np.sqrt(Q[0] * Q[0] + Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3])
+            P = oracle.apply_delta(oracle.quat_to_R(Q / qn), U / nA, P, params.delta_conv).reshape(12)
+            Ec, _ = fit(P)
+        f = params.beta + (1.0 - params.beta) * Ec
+        trace.append([Ebase, nA, omega, v] + list(np.asarray(P).reshape(12)) + [Ec, f * omega, f * v])
+        omega, v = f * omega, f * v
+    q.put((rank, dict(trace=np.array(trace), E=E, n=n)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_point_sharded_ro_equals_unsharded_oracle():
+    """F2b decomposition on 2 gloo ranks: each rank evaluates every candidate on its half of the
+    points, the (S, n) sums are all-reduced, every rank applies the identical update; the in-band
+    counts and |A| equal the unsharded oracle exactly and E / poses within 1e-12 (the sums are fp64
+    here, in a different order; the GPU sums exact fixed-point integers instead)."""
+    import oracle
+    from synth.configs import TrackParams, config_tiny, make_pst
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_points_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c = config_tiny(seed=2)
+    pst = make_pst(2, 37)
+    params = TrackParams(iters=3, stride=2)
+    o = oracle.OracleVolume(c["desc"], c["V"], c["W"]).track(c["depth"], c["intr"], c["T_init"], pst, params)
+    for r in (0, 1):
+        tr = res[r]["trace"]
+        np.testing.assert_array_equal(tr[:, 1], o["trace"][:, 1])
+        np.testing.assert_allclose(tr[:, [0, 16]], o["trace"][:, [0, 16]], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(tr[:, 4:16], o["trace"][:, 4:16], atol=1e-12)
+        np.testing.assert_array_equal(res[r]["n"], o["n"])
+        np.testing.assert_allclose(res[r]["E"], o["E"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_array_equal(res[0]["trace"], res[1]["trace"])

@@ -3,8 +3,10 @@
 // record (record 0 when out of band), in the tracker's work-item order (4 tiles x 16 particles per
 // warp item from one dynamic queue, 4 points per lane batched) -- with no transform and no lerp.
 // The packed index stream (bit 31 in-band, bits 0..30 the record index) is precomputed on the host
-// by tools/gather_replay.py and streamed with evict-first loads (157 MB per iteration at config Q,
-// which makes the ceiling slightly pessimistic).
+// by tools/gather_replay.py and streamed with evict-first loads (157 MB per iteration at config Q),
+// prefetched two particles ahead so that its HBM latency is not part of the replayed chain (r01
+// loaded it in line, which put an HBM round trip in front of every mask -> record pair and made the
+// ceiling pessimistic).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Xcompiler -fPIC -shared -o libreplay.so replay.cu
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -30,10 +32,20 @@ __global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ 
     if (item >= nitems) break;
     const int group = item / nch, chunk = item - group * nch;
     const int k0 = chunk * 16, k1 = min(K, k0 + 16);
+    // the index stream is prefetched two particles ahead (registers), so its HBM latency is off the
+    // replayed chain: what remains is the tracker's own dependent pair, mask word -> record
+    const uint32_t* base = idx + (group * 4) * 32 + lane;
+    uint32_t wn[2][4];
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) wn[d][p] = k0 + d < k1 ? __ldcs(base + (size_t)(k0 + d) * npad + p * 32) : 0u;
     for (int k = k0; k < k1; ++k) {
       uint32_t w[4], mw[4];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) w[p] = __ldcs(idx + (size_t)k * npad + (group * 4 + p) * 32 + lane);
+      for (int p = 0; p < 4; ++p) { w[p] = wn[0][p]; wn[0][p] = wn[1][p]; }
+#pragma unroll
+      for (int p = 0; p < 4; ++p) wn[1][p] = k + 2 < k1 ? __ldcs(base + (size_t)(k + 2) * npad + p * 32) : 0u;
 #pragma unroll
       for (int p = 0; p < 4; ++p) mw[p] = __ldg(mask + ((w[p] & 0x7fffffffu) >> 5));
 #pragma unroll
