@@ -2,20 +2,25 @@
 """Benchmark of the PROFusion tracking-and-fusion hot path on B200 (BASELINE.json metric:
 particle-point TSDF evals/s; ms per 640x480 frame, track + integrate).
 
-One step = one frame of BASELINE config 3 ("Q"): track the 640x480 depth frame (160x120 strided
-points, K = 2048 particles per GPU, 10 iterations, init = GT (+) U+-5 deg/+-5 cm standing in for the
-regression network) against a 512^3 @ 1 cm fp32 TSDF, then integrate the frame at the tracked
-pose.  The TSDF is first built by integrating `--map-frames` frames of the trajectory at GT.
+One step = one frame of BASELINE config 3 ("Q"), as the sequence driver runs it (SURVEY.md §8(c-1)
+O11, reading L25): T_init = P_{t-1} * (GT_{t-1}^-1 GT_t (+) U+-5 deg/+-5 cm) -- the network stand-in
+chained on the previous *tracked* pose, composed on the device (pft_pose_compose) -- then track the
+640x480 depth frame (160x120 strided points, K = 2048 particles per GPU, 10 iterations) against the
+512^3 @ 1 cm fp32 TSDF and integrate the frame at the tracked pose.  The TSDF is the sequence's own:
+frame 0 fused at GT (L24), frames 1 .. map_frames-1 tracked and fused the same way (untimed), then
+the warm-up frames, then the timed frames, all chained.
 
   python bench.py [--gpus N --steps K --warmup W]          # our CUDA path (libpft.so)
-  python bench.py --impl reference [...]                   # the fp64 CPU oracle on a bounded sample
+  python bench.py --impl reference [...]                   # the fp64 CPU oracle, same workload
 
 Multi-GPU (torchrun, one rank per GPU): particles are sharded (K = 2048 * N in total, weak
 scaling), the volume is replicated, and each iteration's per-particle records reach every rank
-through the F2 exchange inside the persistent tracker (P2P stores over NVLink; `--exchange nccl`
-for the ncclAllGather path).  Each frame is replayed as a CUDA graph (`--no-graph` for eager
-calls).  Timing: CUDA events around each step on the launching stream, L2 flushed (256 MiB
-write) between steps outside the events, max over ranks.
+through the F2 exchange inside the persistent tracker (P2P stores over NVLink after a pre-flight;
+`--exchange nccl` for the ncclAllGather path, and the automatic fallback).  The config-W particle
+sweep (K = 4096 / 16384 / 65536 in total, strong scaling) runs at every N, and every rank's poses
+and volume checksum are compared (replica identity).  Timing: CUDA events around each step on the
+launching stream, L2 flushed (256 MiB write) between steps outside the events, max over ranks;
+each frame is replayed as a CUDA graph (`--no-graph` for eager calls).
 """
 import argparse
 import json
@@ -33,9 +38,10 @@ sys.path.insert(0, ROOT)
 
 K_PER_GPU = 2048
 ITERS = 10
-BYTES_PER_EVAL = 32          # 8 trilinear corners x fp32 value
-OPS_PER_EVAL = 32            # algorithmic thread-level operations per particle-point evaluation
-LANES_PER_SM = 128           # 4 SM sub-partitions x 32 lanes, one instruction issue per clock each
+BYTES_PER_EVAL = 32          # one 32-byte cell record gathered per particle-point evaluation
+DP_PER_EVAL = 18             # fp64 pipe instructions per evaluation: 9 DFMA transform + 9 DADD exact floor/fraction
+DFMA_PER_CLK_SM = 61.7       # measured fp64 issue rate per SM (tools/microbench/pipes.cu)
+INTEG_BYTES_PER_VOXEL = {"f32": 16, "f16": 8}   # V + W read and written per updated voxel
 
 
 def parse():
@@ -54,26 +60,39 @@ def parse():
     return p.parse_args()
 
 
+def config_of(args, world, K):
+    """The line's `config` (identical for both arms)."""
+    return {"workload": "Q: 640x480 frames, 160x120 points, K=2048/GPU, 10 iters, 512^3 @1cm fp32 TSDF, "
+                        "track + integrate, init chained on the previous tracked pose (L25)",
+            "particles": K, "iters": ITERS, "volume": "512^3 fp32", "map_frames": args.map_frames,
+            "seed": args.seed, "l2": "flushed (256 MiB write) between steps",
+            "parallelism": f"particles sharded x{world}, volume replicated"}
+
+
 # ---------------------------------------------------------------------------- workload
 def make_workload(args, n_steps, world):
-    from synth.configs import Sequence, init_noise
-    from synth.scene import Intrinsics  # noqa: F401
+    """The sequence (config Q) and per-frame inputs: depth and the network stand-in's relative
+    init rel_t = GT_{t-1}^-1 GT_t (+) U+-5/+-5 (L25).  Frames [0, map_frames) build the map."""
+    from synth.configs import Sequence
     nf = args.map_frames + n_steps
     seq = Sequence("Q", seed=args.seed, n_frames=max(nf, 48), K=K_PER_GPU * world, iters=ITERS)
-    if os.environ.get("PFT_BENCH_PST_ORDER"):
-        from synth.configs import make_pst
-        seq.pst = make_pst(args.seed, seq.K, os.environ["PFT_BENCH_PST_ORDER"])
-    map_depth = [seq.depth(t) for t in range(args.map_frames)]
-    steps = []
-    for i in range(n_steps):
-        t = args.map_frames + i
-        steps.append(dict(t=t, depth=seq.depth(t), T_init=init_noise(args.seed, t, seq.gt[t], 5.0, 5.0)))
-    return seq, map_depth, steps
+    frames = [dict(t=t, depth=seq.depth(t), rel=seq.rel_init(t) if t > 0 else None) for t in range(nf)]
+    return seq, frames
 
 
 def strided_valid(depth, stride, max_depth=8.0):
     d = depth[::stride, ::stride].astype(np.float64) * 0.001
     return int(((depth[::stride, ::stride] > 0) & (d < max_depth)).sum())
+
+
+def ate_cm(poses, gts):
+    d = [np.linalg.norm(np.asarray(a)[:, 3] - np.asarray(g)[:, 3]) for a, g in zip(poses, gts)]
+    return float(np.sqrt(np.mean(np.square(d))) * 100.0)
+
+
+def load_jsonl(name):
+    path = os.path.join(ROOT, "profiles", name)
+    return [json.loads(x) for x in open(path) if x.strip()] if os.path.exists(path) else []
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -143,133 +162,147 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    seq, map_depth, steps_in = make_workload(args, args.warmup + args.steps, world)
+    n_run = args.warmup + args.steps
+    seq, frames = make_workload(args, n_run, world)
     desc, intr, params = seq.desc, seq.intr, seq.params
     K = K_PER_GPU * world
+    M = args.map_frames
 
     vol = pft.Volume(desc, dev)
     vol.reset()
-    for t, d in enumerate(map_depth):
-        vol.integrate(torch.from_numpy(d).to(dev), intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
     exchange = args.exchange
     if world > 1:
-        if exchange == "p2p" and not vol.comm_init_p2p(K):
-            # e.g. GPUs without peer access: every rank detached; fall back to the NCCL path
+        if exchange == "p2p" and not vol.comm_init_p2p(max(K, 65536)):
+            # no peer access, or the pre-flight failed on some rank: every rank detached; NCCL path
             print("bench: P2P exchange unavailable on some rank; using ncclAllGather", file=sys.stderr)
             exchange = "nccl"
         if exchange == "nccl":
             vol.comm_init()
     pst = torch.from_numpy(seq.pst).to(dev)
-    depth_dev = [torch.from_numpy(s["depth"]).to(dev) for s in steps_in]
-    tinit_dev = [torch.from_numpy(s["T_init"]).to(dev) for s in steps_in]
-    n_valid = [strided_valid(s["depth"], params.stride) for s in steps_in]
-    evals = [K * n * ITERS for n in n_valid]
+    stream = torch.cuda.current_stream()
     out = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(K, dtype=torch.float64, device=dev),
                n=torch.empty(K, dtype=torch.int32, device=dev),
                trace=torch.zeros(ITERS, pft.TRACE_DOUBLES, dtype=torch.float64, device=dev))
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-    stream = torch.cuda.current_stream()
+    T_prev = torch.from_numpy(seq.gt[0].copy()).to(dev)     # P_0 = GT_0 (L24)
+    T_init = torch.empty(3, 4, dtype=torch.float64, device=dev)
 
-    def step(i, depth, T_init):
+    def step(depth, rel):
+        """One sequence frame: T_init = P_{t-1} rel_t; track; integrate at the tracked pose; P_t."""
+        pft.pose_compose(T_prev, rel, out=T_init)
         vol.track(depth, intr, T_init, pst, params, out=out)
         vol.integrate(depth, intr, out["T"])
+        T_prev.copy_(out["T"])
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for i in range(args.warmup):
-        step(i, depth_dev[i], tinit_dev[i])
+    # ---- the map: frame 0 fused at GT, frames 1..M-1 tracked and fused (chained), then warm-up
+    vol.integrate(torch.from_numpy(frames[0]["depth"]).to(dev), intr, T_prev)
+    dev_in = {}
+    for t in range(1, M + n_run):
+        dev_in[t] = (torch.from_numpy(frames[t]["depth"]).to(dev), torch.from_numpy(frames[t]["rel"].copy()).to(dev))
+    for t in range(1, M + args.warmup):
+        step(*dev_in[t])
     barrier()
+    idx = list(range(M + args.warmup, M + n_run))          # the timed frames
+    n_valid = {t: strided_valid(frames[t]["depth"], params.stride) for t in idx}
+    evals = [K * n_valid[t] * ITERS for t in idx]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    snap = vol.storage.clone()          # every timed run below starts from this map state and pose
+    snap_T = T_prev.clone()
+    poses = {}                          # run name -> (steps, 3, 4) tracked poses
 
-    # the e2e run below replays the same frames from the same map state (integration changes the map)
-    snap = vol.storage.clone()
+    def restore():
+        vol.storage.copy_(snap)
+        T_prev.copy_(snap_T)
 
-    # ---- device-resident timed region
-    idx = list(range(args.warmup, args.warmup + args.steps))
+    # ---- eager timed run: the per-kernel breakdown (CUDA events around every launch) and launch count
+    Tq = torch.empty(len(idx), 3, 4, dtype=torch.float64, device=dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
+    barrier()
+    pft.profile_start()
+    l0 = pft.launch_count()
+    for j, t in enumerate(idx):
+        flush.zero_()
+        ev[j][0].record(stream)
+        step(*dev_in[t])
+        ev[j][1].record(stream)
+        Tq[j].copy_(out["T"])
+    barrier()
+    launches = pft.launch_count() - l0
+    prof = pft.profile_stop()
+    per_step_eager = [a.elapsed_time(b) for a, b in ev]
+    poses["eager"] = Tq.cpu().numpy()
+    n_chk = int(out["trace"][-1, 21].item())
+    assert n_chk == n_valid[idx[-1]], (n_chk, n_valid[idx[-1]])
+
+    # ---- CUDA-graph replay (the headline): one graph per input-buffer pair, captured once
+    graphs = None
     with Clocks(local) as clk:
-        barrier()
-        pft.profile_start()
-        l0 = pft.launch_count()
-        for j, i in enumerate(idx):
-            flush.zero_()
-            ev[j][0].record(stream)
-            step(i, depth_dev[i], tinit_dev[i])
-            ev[j][1].record(stream)
-        barrier()
-        launches = pft.launch_count() - l0
-        prof = pft.profile_stop()
-        per_step_eager = [a.elapsed_time(b) for a, b in ev]
-        n_chk = int(out["trace"][-1, 21].item())
-        assert n_chk == n_valid[idx[-1]], (n_chk, n_valid[idx[-1]])
-        graphs = None
         if not args.no_graph:
-            # one frame (pft_track + pft_integrate: memsets, the cooperative tracker, the cull and
-            # fusion kernels) captured as a CUDA graph per input-buffer pair, replayed per step;
-            # the eager loop above supplies the per-kernel breakdown and the launch count
-            gd = [torch.empty_like(depth_dev[0]) for _ in range(2)]
-            gt = [torch.empty_like(tinit_dev[0]) for _ in range(2)]
+            gd = [torch.empty_like(dev_in[idx[0]][0]) for _ in range(2)]
+            gr = [torch.empty_like(dev_in[idx[0]][1]) for _ in range(2)]
             graphs = []
             for b in range(2):
-                gd[b].copy_(depth_dev[0])
-                gt[b].copy_(tinit_dev[0])
-                step(0, gd[b], gt[b])  # warm-up on these buffers (the map is restored below)
+                gd[b].copy_(dev_in[idx[0]][0])
+                gr[b].copy_(dev_in[idx[0]][1])
+                step(gd[b], gr[b])             # warm-up on these buffers (state restored below)
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    step(0, gd[b], gt[b])
+                    step(gd[b], gr[b])
                 graphs.append(g)
-            vol.storage.copy_(snap)
+            restore()
             barrier()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
-            for j, i in enumerate(idx):
+            for j, t in enumerate(idx):
                 flush.zero_()
                 ev[j][0].record(stream)
-                gd[0].copy_(depth_dev[i])  # the graph's static inputs (D2D, inside the window)
-                gt[0].copy_(tinit_dev[i])
+                gd[0].copy_(dev_in[t][0])       # the graph's static inputs (D2D, inside the window)
+                gr[0].copy_(dev_in[t][1])
                 graphs[0].replay()
                 ev[j][1].record(stream)
+                Tq[j].copy_(out["T"])
             barrier()
-            n_chk = int(out["trace"][-1, 21].item())
-            assert n_chk == n_valid[idx[-1]], (n_chk, n_valid[idx[-1]])
-    per_step = [a.elapsed_time(b) for a, b in ev]
+            poses["graph"] = Tq.cpu().numpy()
+    per_step = [a.elapsed_time(b) for a, b in ev] if graphs else per_step_eager
     t_ms = sum(per_step)
     t_max = t_ms
     if world > 1:
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    tot_evals = sum(evals[i] for i in idx)
+    tot_evals = sum(evals)
     value = tot_evals / (t_max * 1e-3)
 
-    # ---- end-to-end through the public API with host buffers
-    host_depth = [torch.from_numpy(s["depth"]).pin_memory() for s in steps_in]
-    host_tinit = [torch.from_numpy(s["T_init"]).pin_memory() for s in steps_in]
+    # ---- end-to-end through the public API with host buffers: per step the H2D of the frame's
+    # depth and relative init from pinned memory and the D2H of the tracked pose, inside the window
+    host_depth = {t: torch.from_numpy(frames[t]["depth"]).pin_memory() for t in idx}
+    host_rel = {t: torch.from_numpy(frames[t]["rel"].copy()).pin_memory() for t in idx}
     host_T = [torch.empty(3, 4, dtype=torch.float64).pin_memory() for _ in idx]
-    # double-buffered inputs: frame j+1's H2D runs on a copy stream while frame j computes (a
-    # user's pipeline); every copy lies inside some step's event window (frame 0's inside its own)
-    d_buf = gd if graphs else [torch.empty_like(depth_dev[0]) for _ in range(2)]
-    t_buf = gt if graphs else [torch.empty_like(tinit_dev[0]) for _ in range(2)]
+    d_buf = gd if graphs else [torch.empty_like(dev_in[idx[0]][0]) for _ in range(2)]
+    r_buf = gr if graphs else [torch.empty_like(dev_in[idx[0]][1]) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
     cs = torch.cuda.Stream(device=dev)
 
     def prefetch(j):
-        i, b = idx[j], j & 1
+        # double-buffered inputs: frame j+1's H2D runs on a copy stream while frame j computes (a
+        # user's capture pipeline); every copy lies inside some step's event window
+        t, b = idx[j], j & 1
         with torch.cuda.stream(cs):
             if j >= 2:
                 cs.wait_event(used[b])
-            d_buf[b].copy_(host_depth[i], non_blocking=True)
-            t_buf[b].copy_(host_tinit[i], non_blocking=True)
+            d_buf[b].copy_(host_depth[t], non_blocking=True)
+            r_buf[b].copy_(host_rel[t], non_blocking=True)
             ready[b].record(cs)
 
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in idx]
-    vol.storage.copy_(snap)
-    del snap
+    restore()
     barrier()
-    for j, i in enumerate(idx):
+    for j, t in enumerate(idx):
         flush.zero_()
         ev2[j][0].record(stream)
         if j == 0:
@@ -282,177 +315,202 @@ def run_ours(args):
         if graphs:
             graphs[b].replay()
         else:
-            step(i, d_buf[b], t_buf[b])
+            step(d_buf[b], r_buf[b])
         used[b].record(stream)
         host_T[j].copy_(out["T"], non_blocking=True)
         ev2[j][1].record(stream)
     barrier()
-    # tracked pose vs GT per frame (characterisation of the paper-literal rule)
-    rot_err, tr_err = [], []
-    for j, i in enumerate(idx):
-        Tg, Tt = seq.gt[steps_in[i]["t"]], host_T[j].numpy()
-        c = (np.trace(Tg[:, :3].T @ Tt[:, :3]) - 1.0) / 2.0
-        rot_err.append(float(np.degrees(np.arccos(np.clip(c, -1.0, 1.0)))))
-        tr_err.append(float(np.linalg.norm(Tg[:, 3] - Tt[:, 3]) * 100.0))
+    poses["e2e"] = np.stack([h.numpy() for h in host_T])
     e2e_ms = sum(a.elapsed_time(b) for a, b in ev2)
     if world > 1:
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = host_depth[0].numel() * 2 + 96
+    h2d = host_depth[idx[0]].numel() * 2 + 96
     d2h = 96
+    runs_agree = all(np.array_equal(poses["eager"], p) for p in poses.values())
+    checksum = vol.checksum()
 
-    # ---- roofline of the dominant kernel (k_particle_eval)
-    if prof["eval"][1] > 0:       # multi-launch tracker: k_particle_eval is the dominant kernel
-        kname, (eval_ms, eval_n) = "k_particle_eval", prof["eval"]
-        evals_per_launch = K_PER_GPU * statistics.mean(n_valid[i] for i in idx)
-    else:                         # persistent tracker: one launch per frame holds all 10 iterations
-        kname, (eval_ms, eval_n) = "k_track_persistent (eval+update+centre phases)", prof["track"]
-        evals_per_launch = K_PER_GPU * ITERS * statistics.mean(n_valid[i] for i in idx)
-    avg_launch_s = eval_ms / eval_n * 1e-3
-    gather_gbs = evals_per_launch * BYTES_PER_EVAL / avg_launch_s / 1e9
+    # ---- replica identity (N > 1): every rank's tracked poses (bits) and final volume checksum
+    identity = None
+    if world > 1:
+        bits = torch.from_numpy(poses["e2e"].view(np.int64).ravel().copy()).to(dev)
+        lo, hi = bits.clone(), bits.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        cs_t = torch.tensor([checksum & 0x7FFFFFFFFFFFFFFF, checksum >> 63], dtype=torch.int64, device=dev)
+        cl, ch = cs_t.clone(), cs_t.clone()
+        dist.all_reduce(cl, op=dist.ReduceOp.MIN)
+        dist.all_reduce(ch, op=dist.ReduceOp.MAX)
+        identity = {"identity_ok": bool(torch.equal(lo, hi) and torch.equal(cl, ch)),
+                    "poses_compared": len(idx), "volume_checksum_compared": True}
+
+    # ---- accuracy of the timed frames (characterisation of the paper-literal rule)
+    gts = [seq.gt[t] for t in idx]
+    rot_err, tr_err = [], []
+    for Tt, Tg in zip(poses["e2e"], gts):
+        c = (np.trace(Tg[:, :3].T @ Tt[:, :3]) - 1.0) / 2.0
+        rot_err.append(float(np.degrees(np.arccos(np.clip(c, -1.0, 1.0)))))
+        tr_err.append(float(np.linalg.norm(Tg[:, 3] - Tt[:, 3]) * 100.0))
+
+    # ---- integration work per frame (an untimed replay of the timed frames, reading the counters)
+    integ = {}
+    restore()
+    st_rows = []
+    for t in idx:
+        step(*dev_in[t])
+        st_rows.append(vol.integrate_stats())
+    upd = statistics.mean(r["updated_voxels"] for r in st_rows)
+    esz = getattr(desc, "storage", "f32")
+    ms_int = prof["integrate"][0] / max(prof["integrate"][1], 1)
+    ms_cull = prof["cull"][0] / max(prof["integrate"][1], 1)
+    ms_rec = prof["records"][0] / max(prof["integrate"][1], 1)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    integ = {"updated_voxels_per_frame": upd,
+             "kept_bricks_per_frame": statistics.mean(r["kept_bricks"] for r in st_rows),
+             "free_space_bricks_per_frame": statistics.mean(r["free_bricks"] for r in st_rows),
+             "rebuilt_cell_bricks_per_frame": statistics.mean(r["dirty_cell_bricks"] for r in st_rows),
+             "us_fusion": ms_int * 1e3, "us_cull": ms_cull * 1e3, "us_records": ms_rec * 1e3,
+             "gvox_per_s_fusion_kernel": upd / (ms_int * 1e-3) / 1e9,
+             "gvox_per_s_with_cull_and_records": upd / ((ms_int + ms_cull + ms_rec) * 1e-3) / 1e9,
+             "hbm_frac_fusion_kernel": upd * INTEG_BYTES_PER_VOXEL[esz] / (ms_int * 1e-3) / 1e9 / hbm_peak,
+             "basis": f"{INTEG_BYTES_PER_VOXEL[esz]} B (V + W read + write) per updated voxel (pft_integrate_stats) "
+                      "/ CUDA-event kernel time; peak MEASURED_PEAKS.json hbm_gbs"}
+
+    # ---- roofline of the dominant kernel (the persistent tracker: one launch per frame)
+    if prof["eval"][1] > 0:       # multi-launch tracker: k_particle_eval is the dominant kernel
+        kname, (eval_ms, eval_n) = "k_particle_eval", prof["eval"]
+        evals_per_launch = K_PER_GPU * statistics.mean(n_valid[t] for t in idx)
+    else:
+        kname, (eval_ms, eval_n) = "k_track_persistent (eval+update+centre phases)", prof["track"]
+        evals_per_launch = K_PER_GPU * ITERS * statistics.mean(n_valid[t] for t in idx)
+    avg_launch_s = eval_ms / eval_n * 1e-3
+    kernel_evals_s = evals_per_launch / avg_launch_s
+    gather_gbs = kernel_evals_s * BYTES_PER_EVAL / 1e9
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # issue-slot ceiling from unit counts and clocks: SMs x 128 lanes x f_max
-    alu_peak = n_sm * LANES_PER_SM * sm_mhz * 1e6 / 1e12
-    achieved = evals_per_launch * OPS_PER_EVAL / avg_launch_s / 1e12
+    gth = [r for r in load_jsonl("r02_gather.jsonl") if r.get("test") == "gather32"]
+    band = [r for r in gth if r["footprint_bytes"] == 32 << 20]
+    gather_peak = band[0]["gathers_per_s"] * BYTES_PER_EVAL / 1e9 if band else None
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "eval_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "r02_track_traffic.json")
     if os.path.exists(tf):
         tj = json.load(open(tf))
         traffic = tj.get("dram_bytes_per_eval", 0) * evals_per_launch
-
-    # gather-replay ceiling (tools/gather_replay.py on the bench map): the evaluation's exact mask +
-    # record address stream replayed without arithmetic, next to the tracker on the same frame
+    rep = [x for x in load_jsonl("r02_gather_replay.jsonl") if x.get("init_noise_deg_cm") == 5.0 and x.get("frame") == 12]
     gather_view = None
-    gr = os.path.join(ROOT, "profiles", "r01_gather_replay.jsonl")
-    if os.path.exists(gr):
-        rows = [json.loads(x) for x in open(gr) if x.strip()]
-        ref = [x for x in rows if x.get("init_noise_deg_cm") == 5.0 and x.get("frame") == 12] or rows
-        x = ref[0]
-        gather_view = {"replay_evals_per_s": x["replay_evals_per_s"], "track_evals_per_s": x["track_evals_per_s"],
-                       "frac": x["track_evals_per_s"] / x["replay_evals_per_s"], "inband_frac": x["inband_frac"],
-                       "source": "profiles/r01_gather_replay.jsonl (frame %d, +-%g deg/cm init)" % (
-                           x["frame"], x["init_noise_deg_cm"])}
+    if rep:
+        x = rep[0]
+        gather_view = {"replay_evals_per_s": x["replay_evals_per_s"], "frac": kernel_evals_s / x["replay_evals_per_s"],
+                       "inband_frac": x["inband_frac"],
+                       "source": "profiles/r02_gather_replay.jsonl: the evaluation's exact mask + record address "
+                                 "stream of a bench frame replayed without arithmetic (frame 12, +-5 deg/cm init)"}
+    roofline = {"bound": "gather", "achieved": gather_gbs, "peak": gather_peak, "unit": "GB/s",
+                "frac": gather_gbs / gather_peak if gather_peak else None, "traffic": traffic, "kernel": kname,
+                "basis": f"{BYTES_PER_EVAL} B cell record gathered per particle-point evaluation (the record holds the "
+                         f"8 trilinear corners) x {evals_per_launch:.0f} evaluations/launch / the launch's CUDA-event "
+                         "time; peak = the measured rate of independent random 32-B gathers over a 32 MB (band-sized, "
+                         "L2-resident) footprint, profiles/r02_gather.jsonl (tools/microbench/gather.cu)",
+                "evals_per_s_kernel": kernel_evals_s,
+                "gather_view": gather_view,
+                "hbm_view": {"logical_gather_gbs": gather_gbs, "peak_gbs": hbm_peak, "frac": gather_gbs / hbm_peak,
+                             "note": "served from L2/L1: DRAM bytes are 'traffic'"},
+                "fp64_view": {"dp_instr_per_eval": DP_PER_EVAL, "peak_per_clk_sm": DFMA_PER_CLK_SM,
+                              "frac": kernel_evals_s * DP_PER_EVAL / (n_sm * DFMA_PER_CLK_SM * sm_mhz * 1e6)}}
 
-    # ---- particle sweep (BASELINE config 4 sizes) on the same 512^3 map, one frame, 10 iterations
+    # ---- config-W particle sweep (strong scaling: K in total, sharded over the N ranks), 1 frame
     sweep = {}
-    if world == 1:
-        for Ks in (4096, 16384, 65536):
-            from synth.configs import make_pst
-            pst_s = torch.from_numpy(make_pst(args.seed, Ks)).to(dev)
-            o2 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev),
-                      E=torch.empty(Ks, dtype=torch.float64, device=dev), n=torch.empty(Ks, dtype=torch.int32, device=dev),
-                      trace=None)
-            i0 = idx[0]
-            vol.track(depth_dev[i0], intr, tinit_dev[i0], pst_s, params, out=o2)
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(3):
-                flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                vol.track(depth_dev[i0], intr, tinit_dev[i0], pst_s, params, out=o2)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1))
-            sweep[str(Ks)] = {"evals_per_s": Ks * n_valid[i0] * ITERS / (min(ts) * 1e-3), "ms_track": min(ts)}
-            del pst_s, o2
-        vol._ws = {}
+    t0_ = idx[0]
+    for Ks in (4096, 16384, 65536):
+        from synth.configs import make_pst
+        pst_s = torch.from_numpy(make_pst(args.seed, Ks)).to(dev)
+        o2 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(Ks, dtype=torch.float64, device=dev),
+                  n=torch.empty(Ks, dtype=torch.int32, device=dev), trace=None)
+        restore()
+        pft.pose_compose(T_prev, dev_in[t0_][1], out=T_init)
+        vol.track(dev_in[t0_][0], intr, T_init, pst_s, params, out=o2)
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            vol.track(dev_in[t0_][0], intr, T_init, pst_s, params, out=o2)
+            e1.record(stream)
+            barrier()
+            ts.append(e0.elapsed_time(e1))
+        tm = min(ts)
+        if world > 1:
+            tt = torch.tensor([tm], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tm = float(tt.item())
+        sweep[str(Ks)] = {"evals_per_s": Ks * n_valid[t0_] * ITERS / (tm * 1e-3), "ms_track": tm}
+        del pst_s, o2
+    vol._ws = {}
 
-    # ---- F4 surface extraction on the bench map (NEXT row F4): one full pass over V and W
+    # ---- F4 surface extraction on the final map: reads W everywhere and V where observed
     extract = {}
     if world == 1:
+        restore()
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        lib_ = pft.lib()
-        import ctypes as C
-        lib_.pft_extract_surface(vol.handle, C.c_void_p(0), 0, C.c_void_p(cnt.data_ptr()),
-                                 C.c_void_p(stream.cuda_stream))
-        torch.cuda.synchronize()
-        npts = int(cnt.item())
+        npts = len(vol.extract_surface())
         pts_buf = torch.empty(max(npts, 1), 3, dtype=torch.float64, device=dev)
+        import ctypes as C
         ts = []
         for _ in range(5):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            lib_.pft_extract_surface(vol.handle, C.c_void_p(pts_buf.data_ptr()), npts, C.c_void_p(cnt.data_ptr()),
-                                     C.c_void_p(stream.cuda_stream))
+            pft.check(pft.lib().pft_extract_surface(vol.handle, C.c_void_p(pts_buf.data_ptr()), npts,
+                                                    C.c_void_p(cnt.data_ptr()), C.c_void_p(stream.cuda_stream)))
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ms_x = statistics.median(ts)
-        esz = 4 if getattr(desc, "storage", "f32") == "f32" else 2
-        nbytes = 2 * esz * vol.nvox + 24 * npts  # V + W once, the points written
-        extract = {"ms": ms_x, "points": npts, "algorithmic_bytes": nbytes,
-                   "achieved_gbs": nbytes / (ms_x * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms_x * 1e-3) / 1e9 / hbm_peak}
+        esz_b = 4 if esz == "f32" else 2
+        W_all = vol.download()[1]
+        observed = int((W_all > 0).sum().item())
+        del W_all
+        nbytes = esz_b * vol.nvox + esz_b * observed + 24 * npts
+        extract = {"ms": ms_x, "points": npts, "observed_voxels": observed, "algorithmic_bytes": nbytes,
+                   "achieved_gbs": nbytes / (ms_x * 1e-3) / 1e9, "frac_of_hbm": nbytes / (ms_x * 1e-3) / 1e9 / hbm_peak,
+                   "basis": "W of every voxel + V of every observed voxel read once + 24 B per point written"}
         del pts_buf
 
-    # ---- F2 fused exchange, emulated on this GPU: G rank groups in one persistent launch (same K)
+    # ---- F2 fused exchange and F2b point shards, emulated on this GPU (one frame)
     fused = {}
     if world == 1:
-        i0 = idx[0]
         o3 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(K, dtype=torch.float64, device=dev),
                   n=torch.empty(K, dtype=torch.int32, device=dev), trace=None)
-        for G in (1, 2, 4, 8):
-            vol.comm_init_virtual(G, fused=True)
-            vol.track(depth_dev[i0], intr, tinit_dev[i0], pst, params, out=o3)
+        restore()
+        pft.pose_compose(T_prev, dev_in[t0_][1], out=T_init)
+        for mode, G in [("fused", 1), ("fused", 2), ("fused", 4), ("fused", 8), ("points", 2), ("points", 8)]:
+            vol.comm_init_virtual(G, fused=(mode == "fused"))
+            if mode == "points":
+                vol.set_partition(True)
+            vol.track(dev_in[t0_][0], intr, T_init, pst, params, out=o3)
             torch.cuda.synchronize()
             ts = []
             for _ in range(5):
                 flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                vol.track(depth_dev[i0], intr, tinit_dev[i0], pst, params, out=o3)
+                vol.track(dev_in[t0_][0], intr, T_init, pst, params, out=o3)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            fused[str(G)] = {"ms_track": statistics.median(ts)}
+            fused[f"{mode}_G{G}"] = {"ms_track": statistics.median(ts)}
+            vol.set_partition(False)
         vol.comm_init_virtual(1)
         vol._ws = {}
         del o3
 
-    # ---- config L: 1024^3 @ 5 mm fp16 volume built by integration, K = 4096 track + integrate per frame
+    # ---- config L: 1024^3 @ 5 mm fp16 volume, built by its own sequence, K = 4096 track + integrate
     large = {}
     if world == 1 and not args.no_large:
-        from synth.configs import Sequence
-        sl = Sequence("L", seed=args.seed, n_frames=max(len(map_depth) + 8, 16), K=4096, iters=ITERS)
-        voll = pft.Volume(sl.desc, dev)
-        voll.reset()
-        for t in range(len(map_depth)):
-            voll.integrate(torch.from_numpy(sl.depth(t)).to(dev), sl.intr, torch.from_numpy(sl.gt[t].copy()).to(dev))
-        pst_l = torch.from_numpy(sl.pst).to(dev)
-        frames = [len(map_depth) + f for f in range(6)]
-        dl = [torch.from_numpy(sl.depth(t)).to(dev) for t in frames]
-        from synth.configs import init_noise
-        tl = [torch.from_numpy(init_noise(args.seed, t, sl.gt[t], 5.0, 5.0)).to(dev) for t in frames]
-        ol = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(4096, dtype=torch.float64, device=dev),
-                  n=torch.empty(4096, dtype=torch.int32, device=dev), trace=None)
-        voll.track(dl[0], sl.intr, tl[0], pst_l, sl.params, out=ol)
-        voll.integrate(dl[0], sl.intr, ol["T"])
-        torch.cuda.synchronize()
-        pft.profile_start()
-        ms = []
-        for f in range(1, len(frames)):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            voll.track(dl[f], sl.intr, tl[f], pst_l, sl.params, out=ol)
-            voll.integrate(dl[f], sl.intr, ol["T"])
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        pl = pft.profile_stop()
-        nvl = strided_valid(sl.depth(frames[1]), 4)
-        large = {"workload": "L: 1024^3 @5 mm fp16 V+W, tau 2 cm, K=4096, 10 iters, 640x480",
-                 "ms_per_frame_median": statistics.median(ms),
-                 "evals_per_s": 4096 * nvl * ITERS / (statistics.median(ms) * 1e-3),
-                 "kernel_ms_per_frame": {k: v[0] / len(ms) for k, v in pl.items() if v[1]}}
-        voll.close()
-        del pst_l, dl, tl, ol
+        large = run_large(args, pft, dev, flush, stream)
 
     res = {
         "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
@@ -460,39 +518,35 @@ def run_ours(args):
         "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 transform/decisions, f32 TSDF + lerp, int64 fixed-point sums",
         "data": "synthetic (seeded box room + shaky trajectory, BASELINE config 3)",
-        "config": {"workload": "Q: 640x480 frame, 160x120 points, K=2048/GPU, 10 iters, 512^3 @1cm fp32 TSDF, "
-                               "track + integrate", "particles": K, "points_per_frame": statistics.mean(n_valid),
-                   "iters": ITERS, "volume": "512^3 fp32", "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"particles sharded x{world}, volume replicated"
-                   + (f", {exchange} exchange" if world > 1 else "")},
+        "config": config_of(args, world, K),
+        "points_per_frame": statistics.mean(n_valid.values()),
         "frame_ms": {"median": statistics.median(per_step), "p99": float(np.percentile(per_step, 99)),
                      "max": max(per_step)},
-        "launch": "CUDA graph per frame (track + integrate), replayed" if graphs else "eager library calls",
+        "launch": "CUDA graph per frame (compose + track + integrate), replayed" if graphs else "eager library calls",
         "eager_ms_per_step": sum(per_step_eager) / args.steps,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "e2e": {"value": tot_evals / (e2e_ms * 1e-3), "unit": "evals/s", "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
-                     "frac": achieved / alu_peak, "traffic": traffic, "kernel": kname,
-                     "basis": f"{OPS_PER_EVAL} algorithmic ops/eval x {evals_per_launch:.0f} evals/launch / event time; "
-                              f"peak = {n_sm} SMs x {LANES_PER_SM} lanes x {sm_mhz:.0f} MHz issue slots (DESIGN.md §7)",
-                     "evals_per_s_kernel": evals_per_launch / avg_launch_s,
-                     "gather_view": gather_view,
-                     "hbm_view": {"logical_gather_gbs": gather_gbs, "peak_gbs": hbm_peak, "frac": gather_gbs / hbm_peak,
-                                  "note": f"{BYTES_PER_EVAL} B corner gather/eval, served from L2/L1 (DRAM traffic "
-                                          "is 'traffic'); not the binding resource"}},
+        "runs_agree": runs_agree,
+        "roofline": roofline,
+        "integration": integ,
         "clocks": clk.summary(),
         "particle_sweep": sweep,
-        "fused_exchange_emulation": fused,
         "extract_surface": extract,
+        "fused_exchange_emulation": fused,
         "large_volume": large,
-        "pose_err_vs_gt": {"rot_deg_median": statistics.median(rot_err), "rot_deg_p90": float(np.percentile(rot_err, 90)),
-                           "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),
-                           "note": "paper-literal RO from GT (+) U+-5deg/+-5cm, per frame (SURVEY.md 8(c-5))"},
+        "tracking_accuracy": {"ate_cm_timed_frames": ate_cm(poses["e2e"], gts),
+                              "rot_deg_median": statistics.median(rot_err), "rot_deg_p90": float(np.percentile(rot_err, 90)),
+                              "trans_cm_median": statistics.median(tr_err), "trans_cm_p90": float(np.percentile(tr_err, 90)),
+                              "note": "paper-literal RO, init chained on the previous tracked pose with +-5 deg/cm "
+                                      "stand-in noise (L25); characterisation, SURVEY.md 8(c-5)"},
     }
+    if world > 1:
+        res["scaling_check"] = identity
+        res["config"]["parallelism"] += f", {exchange} exchange"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
-        res["cpu_baseline"] = cpu_baseline(args, seq, map_depth, [steps_in[i] for i in idx])
+        res["cpu_baseline"] = cpu_baseline(args, seq, frames, idx)
     if rank == 0:
         print(json.dumps(res), flush=True)
     vol.close()
@@ -500,12 +554,72 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_large(args, pft, dev, flush, stream):
+    """Config L: its own sequence, frame 0 at GT then tracked + fused frames (chained, K = 4096)."""
+    import torch
+    from synth.configs import Sequence
+    nmap = args.map_frames
+    sl = Sequence("L", seed=args.seed, n_frames=max(nmap + 8, 16), K=4096, iters=ITERS)
+    voll = pft.Volume(sl.desc, dev)
+    voll.reset()
+    pst_l = torch.from_numpy(sl.pst).to(dev)
+    ol = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(4096, dtype=torch.float64, device=dev),
+              n=torch.empty(4096, dtype=torch.int32, device=dev), trace=None)
+    Tp = torch.from_numpy(sl.gt[0].copy()).to(dev)
+    Ti = torch.empty(3, 4, dtype=torch.float64, device=dev)
+    voll.integrate(torch.from_numpy(sl.depth(0)).to(dev), sl.intr, Tp)
+    ms, stats = [], []
+    for t in range(1, nmap + 6):
+        d = torch.from_numpy(sl.depth(t)).to(dev)
+        rel = torch.from_numpy(sl.rel_init(t).copy()).to(dev)
+        timed = t >= nmap + 1
+        if timed:
+            flush.zero_()
+            torch.cuda.synchronize()
+            pft.profile_start()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        pft.pose_compose(Tp, rel, out=Ti)
+        voll.track(d, sl.intr, Ti, pst_l, sl.params, out=ol)
+        voll.integrate(d, sl.intr, ol["T"])
+        Tp.copy_(ol["T"])
+        if timed:
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            pl = pft.profile_stop()
+            stats.append((voll.integrate_stats(), {k: v[0] for k, v in pl.items() if v[1]}))
+    nvl = strided_valid(sl.depth(nmap + 1), 4)
+    kern = {k: statistics.mean(s[1].get(k, 0.0) for s in stats) for k in stats[0][1]}
+    upd = statistics.mean(s[0]["updated_voxels"] for s in stats)
+    voll.close()
+    return {"workload": "L: 1024^3 @5 mm fp16 V+W, tau 2 cm, K=4096, 10 iters, 640x480, chained init",
+            "ms_per_frame_median": statistics.median(ms),
+            "evals_per_s": 4096 * nvl * ITERS / (statistics.median(ms) * 1e-3),
+            "kernel_ms_per_frame": kern,
+            "integration": {"updated_voxels_per_frame": upd,
+                            "gvox_per_s_fusion_kernel": upd / (kern["integrate"] * 1e-3) / 1e9,
+                            "us_fusion": kern["integrate"] * 1e3, "us_cull": kern.get("cull", 0) * 1e3,
+                            "us_records": kern.get("records", 0) * 1e3}}
+
+
 # ---------------------------------------------------------------------------- oracle arms
-def oracle_map(seq, map_depth):
+def oracle_sequence(seq, frames, t_end, nthreads, on_frame=None):
+    """The sequence driver (O11) on the oracle: frame 0 fused at GT, then T_init = P_{t-1} rel_t,
+    track, fuse at the tracked pose, for frames 1 .. t_end-1.  on_frame(t, seconds, result)."""
     import oracle
+    from synth.scene import compose
     ov = oracle.OracleVolume(seq.desc)
-    for t, d in enumerate(map_depth):
-        ov.integrate(d, seq.intr, seq.gt[t])
+    ov.integrate(frames[0]["depth"], seq.intr, seq.gt[0], nthreads=nthreads)
+    P = seq.gt[0]
+    for t in range(1, t_end):
+        t0 = time.perf_counter()
+        T_init = compose(P, frames[t]["rel"])
+        r = ov.track(frames[t]["depth"], seq.intr, T_init, seq.pst, seq.params, nthreads=nthreads)
+        ov.integrate(frames[t]["depth"], seq.intr, r["T"], nthreads=nthreads)
+        P = r["T"]
+        if on_frame and on_frame(t, time.perf_counter() - t0, r):
+            break
     return ov
 
 
@@ -513,29 +627,22 @@ def cores():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_baseline(args, seq, map_depth, steps, budget_s=10.0):
-    """The oracle as it stands, on this host's cores: full RO tracking (K particles, 10 iterations)
-    of consecutive timed frames until ~budget_s of CPU work (>= 1 frame), in evals/s."""
-    ov = oracle_map(seq, map_depth)
-    ev, dt, nf = 0, 0.0, 0
-    for s in steps:
-        t0 = time.perf_counter()
-        r = ov.track(s["depth"], seq.intr, s["T_init"], seq.pst, seq.params, nthreads=cores())
-        dt += time.perf_counter() - t0
-        ev += len(seq.pst) * r["N"] * seq.params.iters
-        nf += 1
-        if dt >= budget_s:
-            break
-    # effective parallelism (SURVEY.md §8(d-6)): the same one-frame track on 1 thread vs all cores,
-    # on a small particle subset
-    s0 = steps[0]
-    sub = seq.pst[:128].copy()
-    t1 = time.perf_counter()
-    ov.track(s0["depth"], seq.intr, s0["T_init"], sub, seq.params, nthreads=1)
-    t1 = time.perf_counter() - t1
-    tn = time.perf_counter()
-    ov.track(s0["depth"], seq.intr, s0["T_init"], sub, seq.params, nthreads=cores())
-    tn = time.perf_counter() - tn
+def cpu_baseline(args, seq, frames, idx, budget_s=12.0):
+    """The oracle as it stands, on this host's cores: the sequence driver (track K particles x 10
+    iterations + fuse per frame) over the first timed frames after building its own map, until
+    ~budget_s of CPU work (>= 1 frame), in evals/s."""
+    acc = {"ev": 0, "dt": 0.0, "nf": 0, "N": 0}
+    first = idx[0]
+
+    def on_frame(t, dt, r):
+        if t < first:
+            return False
+        acc["ev"] += len(seq.pst) * r["N"] * seq.params.iters
+        acc["dt"] += dt
+        acc["nf"] += 1
+        acc["N"] = r["N"]
+        return acc["dt"] >= budget_s
+    oracle_sequence(seq, frames, idx[-1] + 1, cores(), on_frame)
     model = ""
     try:
         for line in open("/proc/cpuinfo"):
@@ -544,43 +651,43 @@ def cpu_baseline(args, seq, map_depth, steps, budget_s=10.0):
                 break
     except OSError:
         pass
-    return {"value": ev / dt, "unit": "evals/s", "cores": cores(), "kind": "oracle",
-            "cpu_model": model, "effective_parallelism": t1 / tn,
-            "sample": f"{nf} frame(s) of full RO tracking ({len(seq.pst)} particles x {seq.params.iters} iterations "
-                      f"x {r['N']} points) on a 512^3 fp32 map fused by the oracle from {len(map_depth)} frames; "
-                      f"{dt:.1f} s"}
+    return {"value": acc["ev"] / acc["dt"], "unit": "evals/s", "cores": cores(), "kind": "oracle", "cpu_model": model,
+            "sample": f"{acc['nf']} timed frame(s) of the chained sequence (track {len(seq.pst)} particles x "
+                      f"{seq.params.iters} iterations x {acc['N']} points + fusion into 512^3 fp32) after the oracle's "
+                      f"own map (frames 0..{first - 1}, untimed); {acc['dt']:.1f} s"}
 
 
 def run_reference(args):
     """The fp64 CPU oracle as the reference arm (this tier has no reference implementation): the
-    same workload per step as our arm (K = 2048 x N particles, 10 iterations, 160x120 points, then
-    fusion into the 512^3 map), on this host's cores.  Under torchrun only rank 0 runs."""
+    same chained sequence and per-step workload as our arm (K = 2048 x N particles, 10 iterations,
+    160x120 points, fusion into the 512^3 map), on this host's cores, each step a frame; the map
+    frames are untimed.  Under torchrun only rank 0 runs."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    seq, map_depth, steps_in = make_workload(args, args.warmup + args.steps, world)
-    ov = oracle_map(seq, map_depth)
+    n_run = args.warmup + args.steps
+    seq, frames = make_workload(args, n_run, world)
+    first_timed = args.map_frames + args.warmup
     per, evs = [], []
-    for i, s in enumerate(steps_in):
-        t0 = time.perf_counter()
-        r = ov.track(s["depth"], seq.intr, s["T_init"], seq.pst, seq.params, nthreads=cores())
-        ov.integrate(s["depth"], seq.intr, r["T"], nthreads=cores())
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
+
+    def on_frame(t, dt, r):
+        if t >= first_timed:
             per.append(dt)
             evs.append(len(seq.pst) * r["N"] * seq.params.iters)
+        return False
+    oracle_sequence(seq, frames, args.map_frames + n_run, cores(), on_frame)
     value = sum(evs) / sum(per)
     res = {"impl": "reference",
            "metric": "particle-point TSDF evals/s (track) with ms per 640x480 frame (track+integrate)",
            "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * sum(per) / len(per), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded box room + shaky trajectory, config 3)",
-           "config": {"workload": f"Q: 640x480 frame, 160x120 points, K={len(seq.pst)}, 10 iters, 512^3 @1cm fp32 "
-                                  "TSDF, track + integrate (full workload per step, fp64 CPU oracle)"},
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded box room + shaky trajectory, BASELINE config 3)",
+           "config": config_of(args, world, len(seq.pst)),
            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores(), "kind": "oracle",
-                            "sample": f"full workload: {len(per)} timed frames (+{args.warmup} warm-up), "
-                                      f"{len(seq.pst)} particles x {seq.params.iters} iterations + fusion"},
+                            "sample": f"full workload: {len(per)} timed frames (+{args.warmup} warm-up, "
+                                      f"{args.map_frames} map frames untimed), {len(seq.pst)} particles x "
+                                      f"{seq.params.iters} iterations + fusion"},
            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
 
