@@ -55,14 +55,15 @@ def report(path, evals=None):
         name = row[h.index("Kernel Name")] if "Kernel Name" in h else "?"
         out.append(f"kernel: {name[:100]}")
         vals = {}
+
+        def num(k):
+            return float(vals.get(k, "0").replace(",", ""))
         for k in KEYS:
             if k in h:
                 i = h.index(k)
                 vals[k] = row[i]
                 out.append(f"  {k:72s} {row[i]:>16s} {units[i]}")
         if evals:
-            def num(k):
-                return float(vals.get(k, "0").replace(",", ""))
             dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
             unit = units[h.index("dram__bytes_read.sum")]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
