@@ -14,7 +14,13 @@ Variants:
   --init pr        P_hat_{t-1} * (GT relative pose (+) U+-5deg/+-5cm): the PR-network stand-in (L25)
   --init ro_alone  P_hat_{t-1} (no relative-pose prior: "RO alone")
   --drop R         drop a fraction R of the frames (seeded; PAPER.md:442, :506 frame-drop protocol)
-  --tracker paper | guard_weighted | schedule   (F3 / F1 variants)
+  --tracker paper | guard_weighted | schedule | topk | schedule_topk | topk_guard   (F3 / F1 variants;
+                   topk = the north_star "top-k" rule with the 32 best members)
+  --init local     no chaining: the map is fused at GT from --map frames, every later frame starts
+                   from GT_t (+) U+-noise and is tracked but not fused -- RO's local convergence alone
+Per frame it also records the pose error of the initial pose and of the RO result against GT, so
+that it shows whether a reading of the update rule actually improves on its initialisation
+(characterisation; the default rule is not changed).
 """
 import argparse
 import dataclasses
@@ -76,10 +82,14 @@ def scene_surface_samples(scene, spacing=0.02, lo=-2.56, hi=2.56):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=60)
-    ap.add_argument("--init", default="pr", choices=["pr", "ro_alone"])
+    ap.add_argument("--init", default="pr", choices=["pr", "ro_alone", "local"])
+    ap.add_argument("--noise", type=float, default=5.0, help="--init local: GT (+) U+-noise deg / cm")
     ap.add_argument("--drop", type=float, default=0.0)
-    ap.add_argument("--tracker", default="paper", choices=["paper", "guard_weighted", "schedule"])
+    ap.add_argument("--tracker", default="paper",
+                    choices=["paper", "guard_weighted", "schedule", "topk", "schedule_topk", "topk_guard"])
+    ap.add_argument("--topk", type=int, default=32)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--map", type=int, default=8, help="--init local: frames fused at GT first")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
 
@@ -99,6 +109,13 @@ def main():
     elif args.tracker == "schedule":
         params = dataclasses.replace(params, **PAPER_SCHEDULE)
         pst = make_pst(args.seed, 10240)
+    elif args.tracker == "topk":
+        params = dataclasses.replace(params, update_rule=2, topk=args.topk)
+    elif args.tracker == "topk_guard":
+        params = dataclasses.replace(params, update_rule=2, topk=args.topk, guard=1)
+    elif args.tracker == "schedule_topk":
+        params = dataclasses.replace(params, update_rule=2, topk=args.topk, **PAPER_SCHEDULE)
+        pst = make_pst(args.seed, 10240)
     keep = np.ones(args.frames, bool)
     if args.drop > 0:
         u = Stream(args.seed, 5).uniform(args.frames)
@@ -110,25 +127,39 @@ def main():
     pst_d = torch.from_numpy(pst).to(dev)
     d0 = seq.depth(0)
     vol.integrate(torch.from_numpy(d0).to(dev), seq.intr, torch.from_numpy(seq.gt[0].copy()).to(dev))
+    if args.init == "local":
+        for t in range(1, args.map):
+            vol.integrate(torch.from_numpy(seq.depth(t)).to(dev), seq.intr, torch.from_numpy(seq.gt[t].copy()).to(dev))
+        frames = np.array([0] + [t for t in frames if t >= args.map])
     est = [seq.gt[0]]
     P_prev, t_prev = seq.gt[0], 0
     t_track = []
+    err_init, err_fin = [], []
+
+    def pose_err(A, B):
+        c = (np.trace(A[:, :3].T @ B[:, :3]) - 1.0) / 2.0
+        return float(np.degrees(np.arccos(np.clip(c, -1.0, 1.0)))), float(np.linalg.norm(A[:, 3] - B[:, 3]) * 100.0)
     for t in frames[1:]:
         depth = torch.from_numpy(seq.depth(t)).to(dev)
         if args.init == "pr":
             rel = init_noise(args.seed, int(t), compose(inverse(seq.gt[t_prev]), seq.gt[t]), 5.0, 5.0)
             T_init = compose(P_prev, rel)
+        elif args.init == "local":
+            T_init = init_noise(args.seed, int(t), seq.gt[t], args.noise, args.noise)
         else:
             T_init = P_prev
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         r = vol.track(depth, seq.intr, torch.from_numpy(np.ascontiguousarray(T_init)).to(dev), pst_d, params)
-        vol.integrate(depth, seq.intr, r["T"])
+        if args.init != "local":
+            vol.integrate(depth, seq.intr, r["T"])
         e1.record()
         torch.cuda.synchronize()
         t_track.append(e0.elapsed_time(e1))
         P_prev, t_prev = r["T"].cpu().numpy(), int(t)
         est.append(P_prev)
+        err_init.append(pose_err(np.asarray(T_init), seq.gt[t]))
+        err_fin.append(pose_err(P_prev, seq.gt[t]))
     est = np.stack(est)
     gt = seq.gt[frames]
     raw, aligned = ate_cm(est, gt)
@@ -136,7 +167,14 @@ def main():
     gt_pts = scene_surface_samples(seq.scene)
     acc = float(np.mean(np.abs(seq.scene.sdf(pts))) * 100.0) if len(pts) else None
     comp = float(np.mean(cKDTree(pts).query(gt_pts, k=1)[0] < 0.10) * 100.0) if len(pts) else 0.0
+    ei, ef = np.array(err_init), np.array(err_fin)
+    better = (ef[:, 0] < ei[:, 0]) & (ef[:, 1] < ei[:, 1])
     res = dict(frames=int(len(frames)), init=args.init, drop=args.drop, tracker=args.tracker,
+               noise=args.noise if args.init == "local" else None,
+               topk=int(params.topk) if params.update_rule == 2 else None,
+               init_err_median_deg_cm=[float(np.median(ei[:, 0])), float(np.median(ei[:, 1]))],
+               ro_err_median_deg_cm=[float(np.median(ef[:, 0])), float(np.median(ef[:, 1]))],
+               ro_improves_both_frac=float(better.mean()),
                ate_cm_raw=raw, ate_cm_aligned=aligned, completeness_pct_10cm=comp, accuracy_cm=acc,
                surface_points=int(len(pts)), gt_samples=int(len(gt_pts)),
                ms_per_frame_median=float(np.median(t_track)))
