@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PFT_ABI_VERSION 3
+#define PFT_ABI_VERSION 4
 
 typedef enum {
   PFT_OK = 0,

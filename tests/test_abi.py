@@ -42,7 +42,7 @@ def test_library_is_sm100a(pft):
 
 
 def test_abi_version(pft):
-    assert pft.lib().pft_abi_version() == 3
+    assert pft.lib().pft_abi_version() == 4
 
 
 def _desc(pft, **kw):
