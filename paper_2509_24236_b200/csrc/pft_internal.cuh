@@ -134,6 +134,7 @@ struct TrackLayout {
   size_t acc_local_off, acc_full_off;
   size_t part_off;     // update partials: nblk_upd * kUpdW doubles
   size_t ptab_off;     // persistent path: K x 12 folded candidate poses + K flags
+  size_t mtab_off;     // persistent path: K x 8 member deltas (q, u, pad) for the update
   size_t cpart_off;    // persistent path: per-CTA centre partials (S, n)
   size_t work_off;     // persistent path: per-iteration work counters
   size_t topk_off;     // F3 top-k: per-block candidate lists and the merged result

@@ -214,6 +214,23 @@ __device__ __forceinline__ void member_row(double* row, double E, double Ebase, 
   }
 }
 
+// Same from the member delta precomputed in P1 (the persistent tracker's table: q(4), u(3), pad):
+// identical arithmetic, member_delta's values loaded instead of recomputed.
+__device__ __forceinline__ void member_row_tab(double* row, double E, double Ebase, int rule, const double* mrow) {
+#pragma unroll
+  for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+  if (E < Ebase) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(mrow));
+    const double2 b = __ldcg(reinterpret_cast<const double2*>(mrow) + 1);
+    const double2 c2 = __ldcg(reinterpret_cast<const double2*>(mrow) + 2);
+    const double u2 = __ldcg(mrow + 6);
+    const double w = rule == 1 ? Ebase - E : 1.0;
+    row[0] = w * a.x; row[1] = w * a.y; row[2] = w * b.x; row[3] = w * b.y;
+    row[4] = w * c2.x; row[5] = w * c2.y; row[6] = w * u2;
+    row[7] = 1.0; row[8] = w;
+  }
+}
+
 // ---- F3 top-k: (E_k, k) keys.  E >= 0 doubles order like their bit patterns; non-members get ~0.
 constexpr int kTopkMax = 32;
 
@@ -1003,7 +1020,7 @@ struct PArgs {
   // at ws on its own GPU otherwise; the o_* are byte offsets inside a region
   char* ws;
   size_t rank_stride;
-  size_t o_state, o_acc, o_ptab, o_pflag, o_upart, o_cpart, o_work;
+  size_t o_state, o_acc, o_ptab, o_pflag, o_upart, o_cpart, o_work, o_mtab;
   size_t o_ckey, o_cidx, o_tkout;  // F3 top-k candidates nblk x kTopkMax (key, index); result Q(4), U(3), n
   // F2 fused exchange (G > 1): xbuf[r] = rank r's exchange buffer (Kpad PartRec records, then
   // kXchgWords counter words), a peer pointer on a real multi-GPU node
@@ -1065,13 +1082,15 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
 template <typename T>
 __device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsigned long long* __restrict__ mask,
                                              const Geom& g, const Points& pts, const double* m, int flag,
-                                             int nb, int lb, unsigned long long& sum, unsigned& cnt) {
+                                             int nb, int lb, unsigned long long& sum, unsigned& cnt,
+                                             const double* pre = nullptr) {
   const int per = (pts.npad + nb - 1) / nb;
   const int b0 = lb * per, b1 = min(pts.npad, b0 + per);
   for (int base = b0; base < b1; base += kThreads) {
     const int i = base + threadIdx.x;
     double px[1] = {0.0}, py[1] = {0.0}, pz[1] = {0.0};
-    if (i < b1) { px[0] = __ldcg(pts.x + i); py[0] = __ldcg(pts.y + i); pz[0] = __ldcg(pts.z + i); }
+    if (pre && base == b0) { px[0] = pre[0]; py[0] = pre[1]; pz[0] = pre[2]; }  // first pass, loaded early
+    else if (i < b1) { px[0] = __ldcg(pts.x + i); py[0] = __ldcg(pts.y + i); pz[0] = __ldcg(pts.z + i); }
     double mm[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) mm[q] = m[q];
@@ -1146,6 +1165,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
   TrackState* st = (TrackState*)(wsb + a.o_state);
   PartRec* const acc = (PartRec*)(wsb + a.o_acc);                // this rank's shard accumulators
   double* const ptab = (double*)(wsb + a.o_ptab);
+  double* const mtab = (double*)(wsb + a.o_mtab);  // member deltas (q, u) of all K_i rows
   int* const pflag = (int*)(wsb + a.o_pflag);
   double* const upart = (double*)(wsb + a.o_upart);
   unsigned long long* const cpart = (unsigned long long*)(wsb + a.o_cpart);
@@ -1249,14 +1269,31 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
       __syncthreads();
     }
     PFT_TMARK(0);
-    // ---- P1: candidate-pose table (K_i rows)
-    for (int k = kb + lb * kThreads + tid; k < min(Ki, kb + kloc); k += nb * kThreads) {
+    // ---- P1: candidate-pose table (K_i rows), interleaved over all CTAs (row kb + tid*nb + lb):
+    // each pose is a ~2500-cycle fp64 chain, so K = 2048 rows on 296 CTAs x ~7 threads is one
+    // chain's latency, where contiguous 256-row slices put them all on 8 SMs' fp64 pipes
+    for (int k = kb + tid * nb + lb; k < min(Ki, kb + kloc); k += nb * kThreads) {
       double m[12];
       pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
       double2* row = (double2*)(ptab + 12 * (size_t)k);
 #pragma unroll
       for (int q = 0; q < 6; ++q) row[q] = make_double2(m[2 * q], m[2 * q + 1]);
     }
+    // and, on threads the pose rows leave idle, the member deltas (q_k, u_k) of all K_i rows for P3
+    // (plain / weighted mean), so P3 loads them instead of running the sincos chain on the 256-row
+    // blocks' few SMs
+#ifdef PFT_MEMBER_TABLE
+    if (a.rule != 2)
+      for (int k = (kThreads - 1 - tid) * nb + lb; k < Ki; k += nb * kThreads) {
+        double q[4], u[3];
+        member_delta(a.pst + 6 * (size_t)k, sState[0], sState[1], q, u);
+        double2* mrow = (double2*)(mtab + 8 * (size_t)k);
+        mrow[0] = make_double2(q[0], q[1]);
+        mrow[1] = make_double2(q[2], q[3]);
+        mrow[2] = make_double2(u[0], u[1]);
+        mtab[8 * (size_t)k + 6] = u[2];
+      }
+#endif
     grid_barrier(st, gen, nb, a.watchdog_ns);
     PFT_TMARK(1);
     // F2: this rank's shard of the K_i particles, local rows [0, Ks) = global rows [kb, kb + Ks)
@@ -1422,7 +1459,11 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         if (a.rule == 2) {
           if (E < Ebase) key = (unsigned long long)__double_as_longlong(E);
         } else {
+#ifdef PFT_MEMBER_TABLE
+          member_row_tab(row, E, Ebase, a.rule, mtab + 8 * (size_t)k);
+#else
           member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
+#endif
         }
         if (G == 1) {
           acc[k].S = 0ull;
@@ -1438,6 +1479,12 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
         if (tid < kUpdW) upart[b * kUpdW + tid] = red[tid][0];
         __syncthreads();
       }
+    }
+    // the centre slice's first-pass points, loaded now: their L2 round trip overlaps the barrier
+    double cpre[3] = {0.0, 0.0, 0.0};
+    {
+      const int per = (pts.npad + nb - 1) / nb, i = lb * per + tid;
+      if (i < min(pts.npad, lb * per + per)) { cpre[0] = __ldcg(pts.x + i); cpre[1] = __ldcg(pts.y + i); cpre[2] = __ldcg(pts.z + i); }
     }
     grid_barrier(st, gen, nb, a.watchdog_ns);
     PFT_TMARK(3);
@@ -1477,7 +1524,7 @@ __global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
+      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt, cpre);
       unsigned long long S;
       unsigned n;
       block_total(sum, cnt, sS, sNw, S, n);
@@ -1602,6 +1649,7 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   L->cacc_off = off; off = align_up(off + 2 * sizeof(unsigned long long), 256);
   L->part_off = off; off = align_up(off + kUpdW * sizeof(double) * (size_t)L->nblk_upd, 256);
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
+  L->mtab_off = off; off = align_up(off + 8 * sizeof(double) * (size_t)nparticles, 256);
   L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
   L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024 + sizeof(unsigned long long) * 148 * 8, 256);
   L->topk_off = off;
@@ -1811,6 +1859,7 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.o_acc = c.L.acc_local_off;
   pa.o_ptab = c.L.ptab_off;
   pa.o_pflag = c.L.ptab_off + 12 * sizeof(double) * (size_t)Kp;
+  pa.o_mtab = c.L.mtab_off;
   pa.o_upart = c.L.part_off;
   pa.o_cpart = c.L.cpart_off;
   pa.o_work = c.L.work_off;
