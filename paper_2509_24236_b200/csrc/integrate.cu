@@ -13,12 +13,14 @@
 // margins) compacts the 4^3 bricks that can contain an updated voxel; the fusion kernel then
 // sweeps only those bricks, 64 consecutive elements (one brick = 2 x 128 B lines per array
 // at fp32) per pair of warps, fully coalesced.  The full sweep is kept for verification.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <utility>
 #include <vector>
 
 #include "pft_internal.cuh"
+#include "records.cuh"
 
 namespace pft {
 
@@ -152,9 +154,10 @@ __global__ __launch_bounds__(256) void k_integrate_sweep(Geom g, Intr K, const u
 // ~min over the tile's pixels of (valid ? raw : 0)} (validity is the exact fp64 test of O1,
 // raw > 0 and raw * unit < max_depth; the minimum is stored complemented so that both halves are
 // maxima with identity 0).  A box's footprint is bounded by at most 4 x 4 tiles of the finest
-// level whose tiles it spans at most 4 of per axis: 16 independent loads in one round trip.
+// level whose tiles it spans at most 4 of per axis: 16 independent loads in one round trip.  Four
+// levels (8..64 px tiles): a footprint wider than 4 x 64 px is kept without a test.
 constexpr int kTile = 8;
-constexpr int kLevels = 6;  // tiles of 8, 16, 32, 64, 128, 256 pixels
+constexpr int kLevels = 4;
 struct Pyr {
   int W, H;   // image size; level l has nx(l) x ny(l) tiles starting at element off(l)
   int total;  // elements (uint2) of all levels
@@ -175,37 +178,34 @@ static Pyr make_pyr(int W, int H) {
 
 __device__ __forceinline__ uint2 tmax(uint2 a, uint2 b) { return make_uint2(max(a.x, b.x), max(a.y, b.y)); }
 
-// Frame preparation (one launch): CTAs [0, nreg) build the depth pyramid, one per 64 x 64-pixel
-// region (a level-3 tile): its 64 level-0 tiles by warps, levels 1-3 from shared memory, levels 4-5
-// by atomicMax (zeroed beforehand); the remaining CTAs compute the axis tables.
-__global__ __launch_bounds__(256) void k_frame_prep(Intr K, double max_depth, const uint16_t* __restrict__ depth,
-                                                    uint2* __restrict__ tiles, Pyr P, int nreg, Geom g,
-                                                    const double* __restrict__ Tdev, double4* __restrict__ tab) {
-  if ((int)blockIdx.x >= nreg) {
-    const int n0 = 4 * g.nbx, n1 = 4 * g.nby, n2 = 4 * g.nbz;
-    const int e = ((int)blockIdx.x - nreg) * 256 + threadIdx.x;
-    if (e < n0 + n1 + n2) {
-      const int a = e < n0 ? 0 : (e < n0 + n1 ? 1 : 2);
-      const int i = e - (a == 0 ? 0 : (a == 1 ? n0 : n0 + n1));
-      const double o = a == 0 ? g.ox : (a == 1 ? g.oy : g.oz);
-      const double gw = __dadd_rn(o, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
-      const double d = __dsub_rn(gw, Tdev[3 + 4 * a]);
-      tab[e] = make_double4(__dmul_rn(Tdev[4 * a], d), __dmul_rn(Tdev[4 * a + 1], d), __dmul_rn(Tdev[4 * a + 2], d),
-                            0.0);
-    }
-    return;
-  }
-  __shared__ uint2 s0[64], s1[16], s2[4];
+// Axis tables (fuse_voxel): entry e of the three axes' 4*(nbx+nby+nbz) entries.
+__device__ __forceinline__ void axis_entry(const Geom& g, const double* __restrict__ Tdev, double4* __restrict__ tab,
+                                           int e) {
+  const int n0 = 4 * g.nbx, n1 = 4 * g.nby, n2 = 4 * g.nbz;
+  if (e >= n0 + n1 + n2) return;
+  const int a = e < n0 ? 0 : (e < n0 + n1 ? 1 : 2);
+  const int i = e - (a == 0 ? 0 : (a == 1 ? n0 : n0 + n1));
+  const double o = a == 0 ? g.ox : (a == 1 ? g.oy : g.oz);
+  const double gw = __dadd_rn(o, __dmul_rn(g.voxel, __dadd_rn((double)i, 0.5)));
+  const double d = __dsub_rn(gw, Tdev[3 + 4 * a]);
+  tab[e] = make_double4(__dmul_rn(Tdev[4 * a], d), __dmul_rn(Tdev[4 * a + 1], d), __dmul_rn(Tdev[4 * a + 2], d), 0.0);
+}
+
+// Frame preparation of one 64 x 64-pixel region (a level-3 tile; the whole CTA): its 64 level-0 tiles
+// by warps, levels 1-3 from shared memory.
+__device__ __forceinline__ void prep_region(const Intr& K, double max_depth, const uint16_t* __restrict__ depth,
+                                            uint2* __restrict__ tiles, const Pyr& P, int v, uint2* s0, uint2* s1,
+                                            uint2* s2) {
   const int nx3 = P.nx(3);
-  const int rx = (int)blockIdx.x % nx3, ry = (int)blockIdx.x / nx3;
+  const int rx = v % nx3, ry = v / nx3;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nx0 = P.nx(0), ny0 = P.ny(0);
   int raw[16];  // all 16 pixel loads of this lane in flight together; -1: outside the image
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int ti = warp * 8 + (q >> 1), p = lane + 32 * (q & 1);
-    const int u = (rx * 8 + (ti & 7)) * kTile + (p & 7), v = (ry * 8 + (ti >> 3)) * kTile + (p >> 3);
-    raw[q] = (u < K.W && v < K.H) ? (int)__ldg(depth + (size_t)v * K.W + u) : -1;
+    const int u = (rx * 8 + (ti & 7)) * kTile + (p & 7), vv = (ry * 8 + (ti >> 3)) * kTile + (p >> 3);
+    raw[q] = (u < K.W && vv < K.H) ? (int)__ldg(depth + (size_t)vv * K.W + u) : -1;
   }
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -245,14 +245,21 @@ __global__ __launch_bounds__(256) void k_frame_prep(Intr K, double max_depth, co
     if (X < P.nx(2) && Y < P.ny(2)) tiles[P.off(2) + Y * P.nx(2) + X] = m;
   }
   __syncthreads();
-  if (t == 0) {
-    const uint2 m = tmax(tmax(s2[0], s2[1]), tmax(s2[2], s2[3]));
-    tiles[P.off(3) + ry * nx3 + rx] = m;
-    uint2* t4 = tiles + P.off(4) + (ry >> 1) * P.nx(4) + (rx >> 1);
-    uint2* t5 = tiles + P.off(5) + (ry >> 2) * P.nx(5) + (rx >> 2);
-    if (m.x) { atomicMax(&t4->x, m.x); atomicMax(&t5->x, m.x); }
-    if (m.y) { atomicMax(&t4->y, m.y); atomicMax(&t5->y, m.y); }
+  if (t == 0) tiles[P.off(3) + ry * nx3 + rx] = tmax(tmax(s2[0], s2[1]), tmax(s2[2], s2[3]));
+  __syncthreads();  // (s0..s2 are reused by the next region of this CTA)
+}
+
+// Frame preparation, one launch: CTAs [0, nreg) build the pyramid (one region each), the remaining
+// CTAs compute the axis tables (the full sweep: tables only, nreg = 0).
+__global__ __launch_bounds__(256) void k_frame_prep(Intr K, double max_depth, const uint16_t* __restrict__ depth,
+                                                    uint2* __restrict__ tiles, Pyr P, int nreg, Geom g,
+                                                    const double* __restrict__ Tdev, double4* __restrict__ tab) {
+  __shared__ uint2 s0[64], s1[16], s2[4];
+  if ((int)blockIdx.x >= nreg) {
+    axis_entry(g, Tdev, tab, ((int)blockIdx.x - nreg) * 256 + threadIdx.x);
+    return;
   }
+  prep_region(K, max_depth, depth, tiles, P, blockIdx.x, s0, s1, s2);
 }
 
 // Conservative classification of a box of voxel centres given by its centre (world, fp64) and
@@ -332,35 +339,36 @@ __device__ __forceinline__ void append_warp(bool keep, uint32_t v, uint32_t* __r
 constexpr int kSuper = 4;  // super-brick = 4^3 bricks = 16^3 voxels
 
 // Level 1: one thread per super-brick (its 16 tile loads issued together); survivors appended
-// warp-aggregated.
-__global__ __launch_bounds__(256) void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev,
-                                                    const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy, int nsz,
-                                                    uint32_t* __restrict__ slist, uint32_t* __restrict__ scount) {
+// warp-aggregated.  Whole warps iterate together (warp w of nwarps takes super-bricks 32 w + lane, ...).
+__device__ __forceinline__ void cull_super_pass(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
+                                                const uint2* __restrict__ tiles, const Pyr& P, int nsx, int nsy, int nsz,
+                                                uint32_t* __restrict__ slist, uint32_t* __restrict__ scount,
+                                                uint32_t warp, uint32_t nwarps) {
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
-  const uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x;
-  int c = kCull;
-  if (sb < ns) {
-    const int sx = (int)(sb % (uint32_t)nsx);
-    const uint32_t r = sb / (uint32_t)nsx;
-    const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
-    // voxel-centre box of the super-brick: voxels [16 s, 16 s + 15] per axis
-    c = box_class(g, K, Tdev, tiles, P, g.ox + g.voxel * (16.0 * sx + 8.0), g.oy + g.voxel * (16.0 * sy + 8.0),
-                  g.oz + g.voxel * (16.0 * sz + 8.0), (float)(7.5 * 1.7320508 * g.voxel) + 1e-3f, -1);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b0 = warp * 32; b0 < ns; b0 += nwarps * 32) {
+    const uint32_t sb = b0 + lane;
+    int c = kCull;
+    if (sb < ns) {
+      const int sx = (int)(sb % (uint32_t)nsx);
+      const uint32_t r = sb / (uint32_t)nsx;
+      const int sy = (int)(r % (uint32_t)nsy), sz = (int)(r / (uint32_t)nsy);
+      // voxel-centre box of the super-brick: voxels [16 s, 16 s + 15] per axis
+      c = box_class(g, K, Tdev, tiles, P, g.ox + g.voxel * (16.0 * sx + 8.0), g.oy + g.voxel * (16.0 * sy + 8.0),
+                    g.oz + g.voxel * (16.0 * sz + 8.0), (float)(7.5 * 1.7320508 * g.voxel) + 1e-3f, -1);
+    }
+    append_warp(c != kCull, sb, slist, scount);
   }
-  append_warp(c != kCull, sb, slist, scount);
 }
 
-// Level 2: one warp per surviving super-brick, two of its 64 bricks per lane; warp-stride loop over
-// the survivors with a grid of co-resident CTAs.
-__global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const double* __restrict__ Tdev,
-                                                     const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy,
-                                                     const uint32_t* __restrict__ slist,
-                                                     const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
-                                                     uint32_t* __restrict__ count, uint32_t* __restrict__ nfree_out) {
-  const uint32_t n = *scount;
+// Level 2: one warp per surviving super-brick, two of its 64 bricks per lane.
+__device__ __forceinline__ void cull_bricks_pass(const Geom& g, const Intr& K, const double* __restrict__ Tdev,
+                                                 const uint2* __restrict__ tiles, const Pyr& P, int nsx, int nsy,
+                                                 const uint32_t* __restrict__ slist, uint32_t n,
+                                                 uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                                                 uint32_t* __restrict__ nfree_out, uint32_t warp, uint32_t nwarps) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < n; li += nw) {
+  for (uint32_t li = warp; li < n; li += nwarps) {
     const uint32_t sb = slist[li];
     const int sx = (int)(sb % (uint32_t)nsx);
     const uint32_t r = sb / (uint32_t)nsx;
@@ -380,6 +388,22 @@ __global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const doubl
   }
 }
 
+__global__ __launch_bounds__(256) void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev,
+                                                    const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy, int nsz,
+                                                    uint32_t* __restrict__ slist, uint32_t* __restrict__ scount) {
+  cull_super_pass(g, K, Tdev, tiles, P, nsx, nsy, nsz, slist, scount, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                  (gridDim.x * blockDim.x) >> 5);
+}
+
+__global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const double* __restrict__ Tdev,
+                                                     const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy,
+                                                     const uint32_t* __restrict__ slist,
+                                                     const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
+                                                     uint32_t* __restrict__ count, uint32_t* __restrict__ nfree_out) {
+  cull_bricks_pass(g, K, Tdev, tiles, P, nsx, nsy, slist, *scount, list, count, nfree_out,
+                   (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
+}
+
 // A FREE-class voxel (box_class): v_new = 1, so V' = (V W + 1)/(W + 1) (= 1 exactly when V = 1, see
 // fuse_voxel) and W' = min(W + 1, W_max), each rounded once -- the definition's update without its
 // projection, whose every possible outcome was proven to be "updated with v_new = 1".
@@ -396,25 +420,21 @@ __device__ __forceinline__ bool fuse_free(const Geom& g, T Vs, T Ws, T* __restri
 }
 
 // Sweep of the compacted bricks: a warp covers half a brick (one voxel per lane), 4 bricks per
-// 256-thread CTA and iteration, CTA-stride over the list.  The next brick's list entry is loaded one
-// iteration ahead and the voxel's stored value/weight before the projection chain (their addresses
-// depend only on the list).
+// 256-thread CTA and iteration, CTA-stride over the list (CTAs block, block + nblocks, ...).  The
+// next brick's list entry is loaded one iteration ahead and the voxel's stored value/weight before
+// the projection chain (their addresses depend only on the list).  *sUpd (shared, zeroed by the
+// caller) collects the CTA's updated voxels.
 template <typename T>
-__global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const uint16_t* __restrict__ depth,
-                                                        const double4* __restrict__ tab, const uint32_t* __restrict__ list,
-                                                        const uint32_t* __restrict__ count, T* __restrict__ V,
-                                                        T* __restrict__ W, uint32_t* __restrict__ dirty,
-                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount,
-                                                        unsigned long long* __restrict__ nupd) {
-  __shared__ unsigned sUpd;
-  if (threadIdx.x == 0) sUpd = 0u;
-  __syncthreads();
+__device__ __forceinline__ void fuse_pass(const Geom& g, const Intr& K, const uint16_t* __restrict__ depth,
+                                          const double4* __restrict__ tab, const uint32_t* __restrict__ list, uint32_t n,
+                                          T* __restrict__ V, T* __restrict__ W, uint32_t* __restrict__ dirty,
+                                          uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount, unsigned* sUpd,
+                                          uint32_t block, uint32_t nblocks) {
   unsigned upd = 0u;  // voxels this thread updated (work counter, pft_integrate_stats)
   const int n0 = 4 * g.nbx, n1 = 4 * g.nby;
-  const uint32_t n = *count;
   const uint32_t w = threadIdx.x & 63;
-  const uint32_t step = gridDim.x * 4;
-  uint32_t li = blockIdx.x * 4 + (threadIdx.x >> 6);
+  const uint32_t step = nblocks * 4;
+  uint32_t li = block * 4 + (threadIdx.x >> 6);
   uint32_t e = li < n ? __ldg(list + li) : 0u;
   for (; li < n; li += step) {
     const int bx = (int)(e & 1023u), by = (int)((e >> 10) & 1023u), bz = (int)((e >> 20) & 1023u);
@@ -445,9 +465,82 @@ __global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const ui
     if (nbm) mark_dirty_cells_warp(g, bx, by, bz, nbm, dirty, dlist, dcount);  // warp-uniform
   }
   upd = __reduce_add_sync(0xffffffffu, upd);
-  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(&sUpd, upd);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(sUpd, upd);
+}
+
+template <typename T>
+__global__ __launch_bounds__(256) void k_integrate_list(Geom g, Intr K, const uint16_t* __restrict__ depth,
+                                                        const double4* __restrict__ tab, const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ count, T* __restrict__ V,
+                                                        T* __restrict__ W, uint32_t* __restrict__ dirty,
+                                                        uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount,
+                                                        unsigned long long* __restrict__ nupd) {
+  __shared__ unsigned sUpd;
+  if (threadIdx.x == 0) sUpd = 0u;
+  __syncthreads();
+  fuse_pass<T>(g, K, depth, tab, list, *count, V, W, dirty, dlist, dcount, &sUpd, blockIdx.x, gridDim.x);
   __syncthreads();
   if (threadIdx.x == 0 && sUpd) atomicAdd(nupd, (unsigned long long)sUpd);
+}
+
+// ---- the whole culled integration in ONE cooperative launch (co-resident CTAs): frame preparation
+// | cull level 1 | cull level 2 | fusion | record refresh, separated by a grid barrier (a monotone
+// arrival counter in the volume scratch, zeroed with the frame's counters) instead of 4 kernel
+// boundaries.  Same device functions as the separate kernels (the fallback), so the same bits.
+struct FusedArgs {
+  Geom g;
+  Intr K;
+  Pyr P;
+  const uint16_t* depth;
+  const double* T;
+  uint2* tiles;
+  double4* tab;
+  int nreg, ntab, nsx, nsy, nsz;
+  uint32_t *slist, *scount, *list, *count, *dirty, *dlist, *dcount, *nfree;
+  unsigned long long *nupd, *bar;
+  void *V, *W, *R;
+  uint32_t* mask;
+};
+
+__device__ __forceinline__ void coop_barrier(unsigned long long* ctr, unsigned long long& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ __launch_bounds__(256, 5) void k_integrate_fused(FusedArgs a) {
+  __shared__ uint2 s0[64], s1[16], s2[4];
+  __shared__ unsigned sUpd;
+  unsigned long long target = 0ull;
+  if (threadIdx.x == 0) sUpd = 0u;
+  // frame preparation: pyramid regions and axis-table blocks over the CTAs
+  for (int v = blockIdx.x; v < a.nreg + a.ntab; v += gridDim.x) {
+    if (v < a.nreg) prep_region(a.K, a.g.max_depth, a.depth, a.tiles, a.P, v, s0, s1, s2);
+    else axis_entry(a.g, a.T, a.tab, (v - a.nreg) * 256 + threadIdx.x);
+  }
+  coop_barrier(a.bar, target);
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  cull_super_pass(a.g, a.K, a.T, a.tiles, a.P, a.nsx, a.nsy, a.nsz, a.slist, a.scount, warp, nwarps);
+  coop_barrier(a.bar, target);
+  cull_bricks_pass(a.g, a.K, a.T, a.tiles, a.P, a.nsx, a.nsy, a.slist, __ldcg(a.scount), a.list, a.count, a.nfree,
+                   warp, nwarps);
+  coop_barrier(a.bar, target);
+  fuse_pass<T>(a.g, a.K, a.depth, a.tab, a.list, __ldcg(a.count), (T*)a.V, (T*)a.W, a.dirty, a.dlist, a.dcount, &sUpd,
+               blockIdx.x, gridDim.x);
+  __syncthreads();
+  if (threadIdx.x == 0 && sUpd) atomicAdd(a.nupd, (unsigned long long)sUpd);
+  coop_barrier(a.bar, target);
+  records_dirty_pass<T>(a.g, (const T*)a.V, (T*)a.R, a.mask, a.dirty, a.dlist, __ldcg(a.dcount), blockIdx.x, gridDim.x);
 }
 
 __global__ void k_mark_sweep(uint32_t* flag) { *flag = 1u; }
@@ -469,6 +562,17 @@ static int resident_grid(K kern, int threads) {
   const int v = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
   cache.push_back({key, v});
   return v;
+}
+
+// The single cooperative launch is measured slower than the 5 graph-replayed kernels (Q: 69 vs 66 us
+// of kernel time, 1.634 vs 1.626 ms per bench frame; L: 240 vs 200 us -- 740 CTAs through 4 grid
+// barriers cost more than the kernel boundaries they replace), so it is opt-in: PFT_INTEGRATE_FUSED=1.
+static bool use_fused_integrate() {
+  static const bool on = [] {
+    const char* e = getenv("PFT_INTEGRATE_FUSED");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intrinsics* Kp, const double* T,
@@ -503,20 +607,38 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   uint32_t* dirty = (uint32_t*)(vol->base + vol->L.dirty_off);
   uint32_t* dlist = (uint32_t*)(vol->base + vol->L.dlist_off);
   unsigned long long* nupd = (unsigned long long*)(vol->base + vol->L.scratch_off + 256);
-  cudaMemsetAsync(count, 0, 256, st);  // kept, dirty, super-brick counts, updated voxels, free bricks, sweep flag (+64..+319)
-  cudaMemsetAsync(tiles + P.off(4), 0, sizeof(uint2) * (size_t)(P.total - P.off(4)), st);  // levels 4-5 (atomicMax targets)
-  {
-    const int nreg = P.nx(3) * P.ny(3);
-    const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
-    PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<nreg + ntab, 256, 0, st>>>(K, g.max_depth, depth, tiles, P, nreg, g, T, tab));
-  }
+  uint32_t* nfree = (uint32_t*)(vol->base + vol->L.scratch_off + 264);
+  unsigned long long* bar = (unsigned long long*)(vol->base + vol->L.scratch_off + 320);
+  // kept, dirty, super-brick counts, updated voxels, free bricks, sweep flag, barrier (+64..+327)
+  cudaMemsetAsync(count, 0, 264, st);
+  const int nreg = P.nx(3) * P.ny(3);
+  const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
   const int nsx = (g.nbx + kSuper - 1) / kSuper, nsy = (g.nby + kSuper - 1) / kSuper, nsz = (g.nbz + kSuper - 1) / kSuper;
   const uint32_t ns = (uint32_t)nsx * nsy * nsz;
   uint32_t* slist = (uint32_t*)(vol->base + vol->L.slist_off);
   uint32_t* scount = (uint32_t*)(vol->base + vol->L.scratch_off + 192);
+  if (use_fused_integrate()) {
+    FusedArgs fa{g, K, P, depth, T, tiles, tab, nreg, ntab, nsx, nsy, nsz, slist, scount, list, count, dirty, dlist,
+                 dcount, nfree, nupd, bar, vol->base + vol->L.v_off, vol->base + vol->L.w_off, vol->base + vol->L.r_off,
+                 (uint32_t*)(vol->base + vol->L.m_off)};
+    void* args[] = {&fa};
+    cudaError_t e = cudaSuccess;
+    if (vol->esize == 4) {
+      const int grid = resident_grid(k_integrate_fused<float>, 256);
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st,
+                 e = cudaLaunchCooperativeKernel((const void*)k_integrate_fused<float>, dim3(grid), dim3(256), args, 0, st));
+    } else {
+      const int grid = resident_grid(k_integrate_fused<__half>, 256);
+      PFT_LAUNCH(PFT_PROF_INTEGRATE, st,
+                 e = cudaLaunchCooperativeKernel((const void*)k_integrate_fused<__half>, dim3(grid), dim3(256), args, 0, st));
+    }
+    if (e == cudaSuccess) return cuda_check("integrate (fused)");
+    if (e != cudaErrorCooperativeLaunchTooLarge) return fail(PFT_ERR_CUDA, "integrate launch: %s", cudaGetErrorString(e));
+    cudaGetLastError();  // not sticky (SMs partly taken): the separate kernels below, same results
+  }
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<nreg + ntab, 256, 0, st>>>(K, g.max_depth, depth, tiles, P, nreg, g, T, tab));
   PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, nsz, slist, scount));
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count,
-                                                                                   (uint32_t*)(vol->base + vol->L.scratch_off + 264)));
+  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count, nfree));
   // grid = the resident capacity (one wave: no partial second wave of CTAs, the CTA-stride loop
   // balances the bricks)
   const int grid = vol->esize == 4 ? resident_grid(k_integrate_list<float>, 256) : resident_grid(k_integrate_list<__half>, 256);

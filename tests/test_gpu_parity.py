@@ -741,3 +741,21 @@ def test_pose_compose(pft):
         a_dev = T(A)
         pft.pose_compose(a_dev, T(B), out=a_dev)  # in place
         np.testing.assert_allclose(a_dev.cpu().numpy(), compose(A, B), atol=1e-14)
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_integrate_fused_launch_identical(storage, tmp_path):
+    """The opt-in single cooperative integration launch (PFT_INTEGRATE_FUSED=1: pyramid, both cull
+    levels, fusion and record refresh separated by grid barriers) and the default separate kernels
+    run the same device functions: bit-identical volumes, checksums and work counters."""
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_integrate.py")
+    outs = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"{storage}_{mode}.npz")
+        subprocess.check_call([sys.executable, helper, storage, f], env=dict(os.environ, PFT_INTEGRATE_FUSED=mode))
+        outs[mode] = np.load(f)
+    for k in ("V", "W", "stats", "checksum"):
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
+    assert outs["0"]["stats"][:, 2].min() > 1000
