@@ -759,3 +759,50 @@ def test_integrate_fused_launch_identical(storage, tmp_path):
     for k in ("V", "W", "stats", "checksum"):
         assert np.array_equal(outs["0"][k], outs["1"][k]), k
     assert outs["0"]["stats"][:, 2].min() > 1000
+
+
+@pytest.mark.parametrize("case", ["ragged", "far_principal_point", "tiny_image", "huge_image"])
+def test_integrate_edge_cases(pft, case):
+    """Culled integration edge cases against the full sweep and the oracle, bit for bit:
+    ragged volume dims (partial bricks and super-bricks on every axis), a principal point beyond
+    2^19 px (pixel_of's fast path off: every projection decided by the exact division, all outside
+    the image), a 7 x 5 image (a single pyramid tile), and a 2048 x 1536 image (the pyramid does not
+    fit: full-sweep fallback)."""
+    scene = box_room(seed=7)
+    from synth.configs import room_gt_pose
+    T0 = room_gt_pose(scene, 7)
+    if case == "ragged":
+        desc = VolumeDesc(37, 50, 45, 0.06, (-1.11, -1.5, -1.35), 0.15)
+        intr = Intrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    elif case == "far_principal_point":
+        desc = VolumeDesc(64, 64, 64, 0.04, (-1.28, -1.28, -1.28), 0.12)
+        intr = Intrinsics(131.25, 131.25, 79.5, 59.5, 160, 120)
+    elif case == "tiny_image":
+        desc = VolumeDesc(64, 64, 64, 0.04, (-1.28, -1.28, -1.28), 0.12)
+        intr = Intrinsics(3.0, 3.0, 3.0, 2.0, 7, 5)
+    else:
+        desc = VolumeDesc(64, 64, 64, 0.04, (-1.28, -1.28, -1.28), 0.12)
+        intr = Intrinsics(1680.0, 1680.0, 1023.5, 767.5, 2048, 1536)
+    depth = render_depth(scene, intr, T0, Stream(7, 4_000_000))
+    if case == "far_principal_point":
+        intr = Intrinsics(131.25, 131.25, 79.5 + 600000.0, 59.5, 160, 120)
+    vol, vfull = gpu_volume(pft, desc), gpu_volume(pft, desc)
+    ov = oracle.OracleVolume(desc)
+    n_ora = 0
+    for f in range(2):
+        Tf = perturb(T0, [0.0, 0.05 * f, 0.0], [0.0, 0.0, 0.03 * f], 10.0, 10.0)
+        vol.integrate(T(depth), intr, T(Tf))
+        vfull.integrate(T(depth), intr, T(Tf), full_sweep=True)
+        n_ora = ov.integrate(depth, intr, Tf)
+        st = vol.integrate_stats()
+        assert st["updated_voxels"] in (n_ora, -1), (st, n_ora)
+    for v in (vol, vfull):
+        V, W = [x.cpu().numpy() for x in v.download()]
+        assert np.array_equal(storage_bits(V), storage_bits(ov.V)), f"{case}: {int((storage_bits(V) != storage_bits(ov.V)).sum())} values differ"
+        assert np.array_equal(storage_bits(W), storage_bits(ov.W))
+    if case == "far_principal_point":
+        assert (ov.weights_f64() > 0).sum() == 0
+    else:
+        assert (ov.weights_f64() > 0).sum() > 0
+    vol.close()
+    vfull.close()
