@@ -450,6 +450,42 @@ def run_ours(args):
         del pst_s, o2
     vol._ws = {}
 
+    # ---- N > 1: the two partitions over NCCL at config W's smallest K (strong scaling, where the
+    # per-rank work is smallest): particles sharded + all-gather vs points sharded + all-reduce (F2b)
+    partitions = {}
+    if world > 1:
+        from synth.configs import make_pst
+        if exchange == "p2p":
+            vol.comm_detach_p2p()
+            vol.comm_init()
+        Ks = 4096
+        pst_s = torch.from_numpy(make_pst(args.seed, Ks)).to(dev)
+        o2 = dict(T=torch.empty(3, 4, dtype=torch.float64, device=dev), E=torch.empty(Ks, dtype=torch.float64, device=dev),
+                  n=torch.empty(Ks, dtype=torch.int32, device=dev), trace=None)
+        restore()
+        pft.pose_compose(T_prev, dev_in[t0_][1], out=T_init)
+        for name, pts_part in (("particles_allgather", False), ("points_allreduce", True)):
+            vol.set_partition(pts_part)
+            vol.track(dev_in[t0_][0], intr, T_init, pst_s, params, out=o2)
+            ts = []
+            for _ in range(3):
+                flush.zero_()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                vol.track(dev_in[t0_][0], intr, T_init, pst_s, params, out=o2)
+                e1.record(stream)
+                barrier()
+                ts.append(e0.elapsed_time(e1))
+            tm = min(ts)
+            tt = torch.tensor([tm], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tm = float(tt.item())
+            partitions[name] = {"K": Ks, "ms_track": tm, "evals_per_s": Ks * n_valid[t0_] * ITERS / (tm * 1e-3)}
+        vol.set_partition(False)
+        vol._ws = {}
+        del pst_s, o2
+
     # ---- F4 surface extraction on the final map: reads W everywhere and V where observed
     extract = {}
     if world == 1:
@@ -544,6 +580,7 @@ def run_ours(args):
     }
     if world > 1:
         res["scaling_check"] = identity
+        res["partition_sweep_nccl"] = partitions
         res["config"]["parallelism"] += f", {exchange} exchange"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N=1 only
         res["cpu_baseline"] = cpu_baseline(args, seq, frames, idx)
