@@ -992,7 +992,10 @@ __global__ void k_track_finalize(const TrackState* st, int K, double* E_out, int
 //   P5 every CTA: E(P), F3 guard, s-law, stalls, stop rule (identical
 //      decisions); CTA 0 writes the trace.
 // Results are bit-identical to the multi-launch path (same helpers, integer sums, same trees).
-constexpr int kItemTiles = 4;     // 8x4 tiles per warp item (= PPT 4 points per lane)
+#ifndef PFT_ITEM_TILES
+#define PFT_ITEM_TILES 4
+#endif
+constexpr int kItemTiles = PFT_ITEM_TILES;  // 8x4 tiles per warp item (= points per lane)
 #ifndef PFT_ITEM_PARTICLES
 #define PFT_ITEM_PARTICLES 16
 #endif
@@ -1131,7 +1134,10 @@ __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt
 }
 
 template <typename T>
-__global__ __launch_bounds__(kThreads, 2) void k_track_persistent(PArgs a) {
+#ifndef PFT_PERSIST_MINB
+#define PFT_PERSIST_MINB 2
+#endif
+__global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent(PArgs a) {
   // red (update phases) and sPart (evaluation phase) are never live at the same time
   constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
   constexpr size_t kTopBytes = 256 * (sizeof(unsigned long long) + sizeof(int));
