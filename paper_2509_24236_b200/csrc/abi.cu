@@ -263,8 +263,8 @@ pft_status pft_comm_p2p_init(pft_volume* vol, int32_t nranks, int32_t rank, int3
   const size_t kloc = ((size_t)max_particles + nranks - 1) / nranks;
   const size_t rec = (2 * sizeof(pft::PartRec) * kloc * (size_t)nranks + 255) / 256 * 256;
   // records (2 halves), then kMaxFusedRanks round counters + the completed-round word, then
-  // kMaxFusedRanks preflight tokens (pft_comm_p2p_preflight)
-  const size_t bytes = rec + (2 * pft::kMaxFusedRanks + 1) * sizeof(unsigned long long);
+  // kMaxFusedRanks preflight tokens and the preflight result word (pft_comm_p2p_preflight)
+  const size_t bytes = rec + (2 * pft::kMaxFusedRanks + 2) * sizeof(unsigned long long);
   char* p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "exchange buffer (%zu B): %s", bytes, cudaGetErrorString(e));

@@ -2050,13 +2050,12 @@ pft_status p2p_preflight(pft_volume* vol, int timeout_ms, int32_t* ok_out, cudaS
   x.rank = vol->rank;
   for (int q = 0; q < kMaxFusedRanks; ++q) x.xbuf[q] = q < vol->nranks ? vol->xbuf[q] : nullptr;
   x.pre_off = vol->xcnt_off + (kMaxFusedRanks + 1) * sizeof(unsigned long long);
-  int* d_ok = nullptr;
+  // the result word follows the kMaxFusedRanks tokens in this rank's own buffer
+  int* d_ok = (int*)(vol->xown + x.pre_off + kMaxFusedRanks * sizeof(unsigned long long));
   int h_ok = 0;
-  if (cudaMallocAsync((void**)&d_ok, sizeof(int), st) != cudaSuccess) return cuda_check("preflight (alloc)");
   const unsigned long long round = ++vol->preflight_round;
   k_p2p_preflight<<<1, 32, 0, st>>>(x, round, (unsigned long long)timeout_ms * 1000000ull, d_ok);
   cudaMemcpyAsync(&h_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(d_ok, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("preflight");
   *ok_out = h_ok;
   return cuda_check("preflight");
