@@ -243,6 +243,8 @@ pft_status pft_comm_get_unique_id(uint8_t id_out[128]);
 /* Attaches an NCCL communicator (one rank per GPU) to the volume handle; afterwards
  * pft_track shards particles across the nranks GPUs.  The volume is replicated: every rank
  * calls pft_integrate with the same inputs.  The current CUDA device must be this rank's.
+ * nranks = 1 attaches a real single-rank communicator, and pft_track then runs the collective
+ * (multi-launch) path -- the NCCL plumbing exercised on one GPU, results unchanged.
  * PFT_ERR_STATE if virtual ranks or peer exchange buffers are set on the handle.  Collective
  * failures, including asynchronous ones (ncclCommGetAsyncError, polled after each collective),
  * return PFT_ERR_NCCL. */

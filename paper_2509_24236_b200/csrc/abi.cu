@@ -345,7 +345,7 @@ pft_status pft_comm_init(pft_volume* vol, const uint8_t id[128], int32_t nranks,
   if (vol->nccl_comm) return fail(PFT_ERR_STATE, "communicator already initialised");
   if (vol->virtual_ranks || vol->virtual_fused) return fail(PFT_ERR_STATE, "virtual ranks are set (pft_comm_init_virtual*)");
   if (vol->p2p || vol->xown) return fail(PFT_ERR_STATE, "peer exchange buffers are attached (pft_comm_p2p_detach first)");
-  if (nranks == 1) { vol->nranks = 1; vol->rank = 0; return PFT_OK; }
+  // (nranks = 1 attaches a real single-rank communicator: pft_track then runs its collective path)
   Nccl* n = nccl();
   if (!n) return fail(PFT_ERR_NCCL, "libnccl.so.2 not loadable");
   ncclUniqueId uid;

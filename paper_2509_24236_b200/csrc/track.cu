@@ -1645,7 +1645,8 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
     L->sched_set[j] = found;
   }
   // F2b point shards (virtual or NCCL, G > 1): every rank holds all K records
-  L->points_part = vol && vol->partition == PFT_PARTITION_POINTS && nranks > 1 && !vol->virtual_fused && !vol->p2p;
+  L->points_part = vol && vol->partition == PFT_PARTITION_POINTS && (nranks > 1 || vol->nccl_comm) && !vol->virtual_fused &&
+                   !vol->p2p;
   L->kloc = L->points_part ? nparticles : (nparticles + nranks - 1) / nranks;
   L->kfull = L->kloc * nranks;
   L->nblk_upd = (nparticles + 255) / 256;
@@ -1925,7 +1926,8 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
                             const float* pst, int Kp, const pft_track_params* prm, double* T_out, double* E,
                             int32_t* n_out, double* trace) {
   const int G = c.vol->nranks, r = c.vol->rank;
-  if ((G == 1 || c.vol->virtual_fused || c.vol->p2p) && use_persistent() && prm->iters <= 1024) {
+  // (a communicator attached -- even a single-rank one -- selects the collective multi-launch path)
+  if (((G == 1 && !c.vol->nccl_comm) || c.vol->virtual_fused || c.vol->p2p) && use_persistent() && prm->iters <= 1024) {
     const pft_status s = track_persistent<T>(c, depth, K, T_init, pst, Kp, prm, T_out, E, n_out, trace);
     if (s != PFT_ERR_UNSUPPORTED) return s;
     // the cooperative grid does not fit right now (G = 1): same results from the multi-launch path
@@ -1970,7 +1972,7 @@ static pft_status track_run(Launch& c, const uint16_t* depth, const pft_intrinsi
     } else {
       const int k_count = max(0, min(Ki, k_begin + kloc) - k_begin);
       launch_eval<T>(c, 0, pst, k_begin, k_count, prm->delta_conv, nullptr, local, set);
-      if (G > 1) {
+      if (G > 1 || c.vol->nccl_comm) {
         pft_status s = comm_allgather(c.vol, local, full, sizeof(PartRec) * (size_t)kloc, c.st);
         if (s != PFT_OK) return s;
       }

@@ -806,3 +806,28 @@ def test_integrate_edge_cases(pft, case):
         assert (ov.weights_f64() > 0).sum() > 0
     vol.close()
     vfull.close()
+
+
+@pytest.mark.parametrize("partition", ["particles", "points"])
+@pytest.mark.parametrize("cfg", ["single", "tiny_sched", "single_topk"])
+def test_single_rank_nccl_collectives(cfg, partition, tmp_path):
+    """The NCCL plumbing on real collectives: a single-rank communicator (torch.distributed world
+    size 1) makes pft_track take the multi-launch collective path -- ncclAllGather of the particle
+    records, or (F2b) ncclAllReduce of the per-particle and centre fixed-point sums, with the async
+    error polled after each -- and its results equal the plain run bit for bit."""
+    import socket
+    import subprocess
+    import sys
+    helpers = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers")
+    ref = str(tmp_path / "ref.npz")
+    subprocess.check_call([sys.executable, os.path.join(helpers, "run_track.py"), cfg, "1", ref])
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = str(sk.getsockname()[1])
+    sk.close()
+    f = str(tmp_path / "nccl.npz")
+    subprocess.check_call([sys.executable, os.path.join(helpers, "run_nccl1.py"), cfg, partition, f, port])
+    a, b = np.load(ref), np.load(f)
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(a[k], b[k]), k
+    assert int(b["launches"][0]) > 10   # the multi-launch path (kernels + collectives per iteration)
