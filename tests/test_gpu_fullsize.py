@@ -274,3 +274,24 @@ def test_sweep_W_k4096_virtual_shards_G4(sweep):
         assert np.array_equal(a[k], b[k]), k
     _w4096_vs_oracle(b, c, ov, "W K=4096 virtual shards G=4")
     v4.close()
+
+
+def test_sweep_W_k4096_point_shards_G4(sweep):
+    """F2b at full size: config W, K = 4096, 10 iterations with the point-sharded partition over 4
+    virtual ranks (each a contiguous slice of point tiles; sums added across slices): bit-identical
+    to the 1-rank persistent run and equal to the oracle."""
+    import paper_2509_24236_b200 as pft
+    c, vol, ov = sweep
+    pst = T(c["pst"][:4096].copy())
+    params = TrackParams(iters=10, stride=4)
+    a = _np(vol.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params))
+    v4 = pft.Volume(c["desc"], dev())
+    v4.upload(c["V"], c["W"])
+    v4.comm_init_virtual(4)
+    v4.set_partition(True)
+    b = _np(v4.track(T(c["depth"]), c["intr"], T(c["T_init"]), pst, params))
+    torch.cuda.synchronize()
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(a[k], b[k]), k
+    _w4096_vs_oracle(b, c, ov, "W K=4096 point shards G=4")
+    v4.close()
