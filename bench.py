@@ -131,7 +131,7 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -140,13 +140,14 @@ class Clocks:
             try:
                 sm.append(float(f[0]))
                 mx = float(f[1])
+                pw.append(float(f[2]))
             except ValueError:
                 continue
             for n, v in zip(names, f[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "power_w_median": statistics.median(pw) if pw else None, "samples": len(sm)}
 
 
 # ---------------------------------------------------------------------------- our path
@@ -679,7 +680,19 @@ def cpu_baseline(args, seq, frames, idx, budget_s=12.0):
         acc["nf"] += 1
         acc["N"] = r["N"]
         return acc["dt"] >= budget_s
-    oracle_sequence(seq, frames, idx[-1] + 1, cores(), on_frame)
+    ov = oracle_sequence(seq, frames, idx[-1] + 1, cores(), on_frame)
+    # effective parallelism: one frame's track on a 128-particle subset, one
+    # thread vs all cores (sandboxed hosts may expose more cores than they deliver)
+    from synth.scene import compose
+    t = idx[0]
+    T_init = compose(seq.gt[t - 1], frames[t]["rel"])
+    sub = seq.pst[:128].copy()
+    t1 = time.perf_counter()
+    ov.track(frames[t]["depth"], seq.intr, T_init, sub, seq.params, nthreads=1)
+    t1 = time.perf_counter() - t1
+    tn = time.perf_counter()
+    ov.track(frames[t]["depth"], seq.intr, T_init, sub, seq.params, nthreads=cores())
+    tn = time.perf_counter() - tn
     model = ""
     try:
         for line in open("/proc/cpuinfo"):
@@ -689,6 +702,7 @@ def cpu_baseline(args, seq, frames, idx, budget_s=12.0):
     except OSError:
         pass
     return {"value": acc["ev"] / acc["dt"], "unit": "evals/s", "cores": cores(), "kind": "oracle", "cpu_model": model,
+            "effective_parallelism": t1 / tn,
             "sample": f"{acc['nf']} timed frame(s) of the chained sequence (track {len(seq.pst)} particles x "
                       f"{seq.params.iters} iterations x {acc['N']} points + fusion into 512^3 fp32) after the oracle's "
                       f"own map (frames 0..{first - 1}, untimed); {acc['dt']:.1f} s"}
