@@ -13,6 +13,7 @@
 // margins) compacts the 4^3 bricks that can contain an updated voxel; the fusion kernel then
 // sweeps only those bricks, 64 consecutive elements (one brick = 2 x 128 B lines per array
 // at fp32) per pair of warps, fully coalesced.  The full sweep is kept for verification.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -113,6 +114,12 @@ __device__ __forceinline__ bool fuse_voxel(const Geom& g, const Intr& K, const u
   int ui, vi;
   if (!pixel_of(__dmul_rn(K.fx, x), z, rz, K.cx, K.c_small, K.W, ui)) return false;
   if (!pixel_of(__dmul_rn(K.fy, y), z, rz, K.cy, K.c_small, K.H, vi)) return false;
+#ifdef PFT_DEBUG
+  if ((unsigned)ui >= (unsigned)K.W || (unsigned)vi >= (unsigned)K.H) {
+    printf("pft debug: pixel (%d, %d) outside %dx%d\n", ui, vi, K.W, K.H);
+    __trap();
+  }
+#endif
   const uint16_t raw = __ldg(depth + (size_t)vi * K.W + (size_t)ui);
   const double d = __dmul_rn(i2d((int)raw), K.unit);
   if (raw == 0 || !(d < g.max_depth)) return false;
@@ -451,6 +458,12 @@ __device__ __forceinline__ void fuse_pass(const Geom& g, const Intr& K, const ui
     bool changed = false;
     if (i < g.nx && j < g.ny && k < g.nz) {
       const uint32_t o = b * 64u + w;
+#ifdef PFT_DEBUG
+      if (b >= (uint32_t)g.nbx * g.nby * g.nbz || i >= 4 * g.nbx || j >= 4 * g.nby || k >= 4 * g.nbz) {
+        printf("pft debug: bad brick entry %08x (b=%u i=%d j=%d k=%d)\n", e, b, i, j, k);
+        __trap();
+      }
+#endif
       // issued first (independent of the projection chain), streamed past L1 (ld.global.cs) so the
       // axis tables and depth stay L1-resident: Q 37.9 -> 34.3 us, L 165 -> 143 us per frame
       const T Vs = ldcs_t(V + o), Ws = ldcs_t(W + o);

@@ -1,6 +1,8 @@
 // records.cuh — the tracker's cell records and in-band mask, rebuilt from stored V:
 // shared by the volume kernels (volume.cu) and the fused integration kernel (integrate.cu).
 #pragma once
+#include <cstdio>
+
 #include "pft_internal.cuh"
 
 namespace pft {
@@ -58,6 +60,12 @@ __device__ __forceinline__ void records_dirty_pass(const Geom& g, const T* __res
   const uint32_t w = threadIdx.x & 63;
   for (uint32_t li = block * 4 + (threadIdx.x >> 6); li < n; li += nblocks * 4) {
     const uint32_t b = dlist[li];
+#ifdef PFT_DEBUG
+    if (b >= (uint32_t)g.nbx * g.nby * g.nbz) {
+      printf("pft debug: bad dirty cell-brick %u\n", b);
+      __trap();
+    }
+#endif
     const int bx = (int)(b % (uint32_t)g.nbx);
     const uint32_t r = b / (uint32_t)g.nbx;
     const int by = (int)(r % (uint32_t)g.nby), bz = (int)(r / (uint32_t)g.nby);

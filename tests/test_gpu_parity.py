@@ -672,8 +672,9 @@ def test_fused_exchange_counters_follow_the_layout(pft):
 
 def test_debug_build_bounds_checked(tmp_path):
     """The PFT_DEBUG build (every mask / record address bounds- and alignment-checked in the
-    evaluation, a trap on a bad one; DESIGN.md §9's stale-register hazard would show up here) runs
-    config S, a top-k run and the fp16 volume with results bit-identical to the product build."""
+    evaluation, every brick entry, depth pixel and dirty cell-brick in the integration, a trap on a
+    bad one; DESIGN.md §9's stale-register hazard would show up here) runs config S, a top-k run, the
+    fp16 volume and fp32 / fp16 integrations with results bit-identical to the product build."""
     import subprocess
     import sys
     lib = str(tmp_path / "libpft_debug.so")
@@ -687,6 +688,16 @@ def test_debug_build_bounds_checked(tmp_path):
             outs[name] = np.load(f)
         for k in ("T", "E", "n", "trace"):
             assert np.array_equal(outs["prod"][k], outs["debug"][k]), (cfg, k)
+    # and the culled integration (brick entries, pixel indices and dirty cell-bricks checked)
+    ihelper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_integrate.py")
+    for storage in ("f32", "f16"):
+        outs = {}
+        for name, env in (("prod", dict(os.environ)), ("debug", dict(os.environ, PFT_LIB=lib))):
+            f = str(tmp_path / f"integ_{storage}_{name}.npz")
+            subprocess.check_call([sys.executable, ihelper, storage, f], env=env)
+            outs[name] = np.load(f)
+        for k in ("V", "W", "stats", "checksum"):
+            assert np.array_equal(outs["prod"][k], outs["debug"][k]), (storage, k)
 
 
 @pytest.mark.parametrize("G", [2, 3, 8])
