@@ -15,7 +15,13 @@ import oracle
 E_REL, E_ABS = 1e-5, 1e-9
 POSE_M, POSE_RAD = 1e-4, 1e-4
 TIE_MARGIN = 1e-9   # cell decisions: distance of a grid coordinate to an integer (voxel units)
-E_TIE = 1e-8        # fitness decisions: relative distance of E_k to E_base (oracle emargin)
+# fitness decisions: relative distance of E_k to E_base (oracle emargin).  Derived from the GPU's
+# fitness arithmetic (DESIGN.md §6 "Tie handling"): fp32 record coefficients, fp32 lerp and a 2^-23
+# fraction grid give per-evaluation errors of a few 2^-24 |v|; the mean over a candidate's in-band
+# points measured 1.7e-8 relative at most over the 2048 converged candidates of config Q frame 1
+# (test_gpu_fullsize.py::test_fitness_error_budget pins it below E_TIE / 3).  Round 1-2's 1e-8 sat
+# below that measured error and held only because no candidate happened to fall closer.
+E_TIE = 1e-7
 
 
 def close_E(a, b):
@@ -161,6 +167,10 @@ def track_parity(run_gpu, ov, depth, intr, T_init, pst, params, what="", max_tie
         assert len(diff) and np.all(marg < E_TIE), \
             f"{what} iter {i + 1}: |A| gpu={r['trace'][i, 1]} oracle={o['trace'][i, 1]}; particles {diff[:8]} " \
             f"differ with fitness margins {marg[:8]} (not a tie)"
+        # and the GPU's own E_k of a tied particle is within the same bar of the oracle's
+        Eg, Eo = np.asarray(ri["E"], float)[diff], np.asarray(oi["E"], float)[diff]
+        assert np.all(np.abs(Eg - Eo) <= E_TIE * np.abs(Eo)), \
+            f"{what} iter {i + 1}: tied particles {diff[:8]} have E_k gpu={Eg[:4]} oracle={Eo[:4]}"
         force[i, :] = 0
         force[i, :Ki] = m_gpu[:Ki]
         o = ov.track(depth, intr, T_init, pst, params, force=force)

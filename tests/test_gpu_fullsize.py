@@ -10,7 +10,7 @@ import oracle
 from synth.configs import Sequence, TrackParams, config_sweep, init_noise
 from synth.rng import Stream
 from synth.scene import compose, inverse
-from tests.parity import (assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
+from tests.parity import (E_TIE, assert_eval_parity, assert_last_iter_counts, assert_pose_close, assert_trace_parity,
                           close_E, track_parity)
 
 pytestmark = pytest.mark.gpu
@@ -166,6 +166,40 @@ def test_sequence_Q_512_lockstep():
     """Config Q: 512^3 @ 1 cm fp32, K = 2048, 10 iterations, 640x480 frames, the first 31 frames
     (30 tracked) with the chained L25 init; voxel bits at frames 1, 2, 10 and 30; ATE of both."""
     _lockstep("Q", 31, 2048, check_frames={1, 2, 10, 30})
+
+
+def test_fitness_error_budget():
+    """The tie bar E_TIE (tests/parity.py) against the fitness arithmetic it covers: config Q frame 1
+    (map = frame 0 fused at GT, chained L25 init), the oracle's 2048 candidates of its last
+    (converged) iteration -- where near-ties are dense -- evaluated by pft_eval_poses and by the
+    oracle from eq. E: counts exact, and the relative E_k error of every candidate below E_TIE / 3."""
+    import paper_2509_24236_b200 as pft
+    seq = Sequence("Q", seed=1, n_frames=8, K=2048, iters=10)
+    vol = pft.Volume(seq.desc, dev())
+    vol.reset()
+    ov = oracle.OracleVolume(seq.desc)
+    d0 = seq.depth(0)
+    vol.integrate(T(d0), seq.intr, T(seq.gt[0]))
+    ov.integrate(d0, seq.intr, seq.gt[0])
+    depth = seq.depth(1)
+    T_init = compose(seq.gt[0], seq.rel_init(1))
+    o = ov.track(depth, seq.intr, T_init, seq.pst, seq.params)
+    row = o["trace"][seq.params.iters - 2]          # the pose and search size entering the last iteration
+    P, om, v = row[4:16].reshape(3, 4), row[2], row[3]
+    poses = []
+    for k in range(seq.pst.shape[0]):
+        dR, _, u = oracle.delta(seq.pst[k], om, v)
+        poses.append(oracle.apply_delta(dR, u, P, 0))
+    poses = np.stack(poses)
+    e = ov.eval_poses(depth, seq.intr, poses, stride=seq.params.stride)
+    r = vol.eval_poses(T(depth), seq.intr, T(poses), seq.params)
+    torch.cuda.synchronize()
+    E, n = r["E"].cpu().numpy(), r["n"].cpu().numpy()
+    assert_eval_parity(E, n, e, "Q frame 1 last-iteration candidates")
+    ok = n == e["n"]
+    rel = np.abs(E - e["E"])[ok] / np.abs(e["E"][ok])
+    assert ok.sum() >= 2040 and rel.max() < E_TIE / 3, f"max relative E_k error {rel.max():.3e}"
+    vol.close()
 
 
 def test_sequence_L_1024_fp16_lockstep():
