@@ -1378,16 +1378,24 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
           part[k - k0][lane] = (unsigned long long)sum | ((unsigned long long)cnt << 32);
         }
         __syncwarp();
-        // lane j < #particles reduces particle j's row (exact integers) and issues its atomics
-        if (lane < k1 - k0) {
+        // particle j's row is reduced by lanes j and j + 16, half a row each (exact integers),
+        // combined by one shuffle; lane j issues the atomics
+        static_assert(kItemParticles <= 16, "two lanes per particle row");
+        {
+          const int pj = lane & 15, h = lane >> 4;
           unsigned long long S = 0ull;
           unsigned n = 0u;
-          for (int l = 0; l < 32; ++l) {
-            const unsigned long long w = part[lane][l];
-            S += w & 0xffffffffull;
-            n += (unsigned)(w >> 32);
+          if (pj < k1 - k0) {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) {
+              const unsigned long long w = part[pj][h * 16 + l];
+              S += w & 0xffffffffull;
+              n += (unsigned)(w >> 32);
+            }
           }
-          if (n) {
+          S += __shfl_down_sync(0xffffffffu, S, 16);
+          n += __shfl_down_sync(0xffffffffu, n, 16);
+          if (lane < k1 - k0 && n) {
             atomicAdd(&acc[k0 + lane].S, S);
             atomicAdd(&acc[k0 + lane].n, n);
           }
