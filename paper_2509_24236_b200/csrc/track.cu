@@ -987,7 +987,7 @@ __global__ void k_track_finalize(const TrackState* st, int K, double* E_out, int
 //   P0 (once) points of every set, pmax                                    | barrier
 //   B  baseline E(P) on X_j if the set changed (L11)                      | barrier
 //   P1 candidate-pose table (K_j rows, each CTA a slice)                  | barrier
-//   P2 particle x point evaluation: warp-granular items (4 tiles x 16
+//   P2 particle x point evaluation: warp-granular items (6 tiles x 16
 //      particles) handed out by an atomic counter -> no CTA barriers, no
 //      wave tail                                                          | barrier
 //   P3 update partials: 256-particle blocks, the same tree as k_update    | barrier
@@ -997,9 +997,9 @@ __global__ void k_track_finalize(const TrackState* st, int K, double* E_out, int
 //      decisions); CTA 0 writes the trace.
 // Results are bit-identical to the multi-launch path (same helpers, integer sums, same trees).
 #ifndef PFT_ITEM_TILES
-#define PFT_ITEM_TILES 4
+#define PFT_ITEM_TILES 6
 #endif
-constexpr int kItemTiles = PFT_ITEM_TILES;  // 8x4 tiles per warp item (= points per lane)
+constexpr int kItemTiles = PFT_ITEM_TILES;  // 8x4 tiles per warp item (= points per lane); 6: DESIGN.md §7
 #ifndef PFT_ITEM_PARTICLES
 #define PFT_ITEM_PARTICLES 16
 #endif
