@@ -400,14 +400,17 @@ def run_ours(args):
     if os.path.exists(tf):
         tj = json.load(open(tf))
         traffic = tj.get("dram_bytes_per_eval", 0) * evals_per_launch
-    rep = [x for x in load_jsonl("r02_gather_replay.jsonl") if x.get("init_noise_deg_cm") == 5.0 and x.get("frame") == 12]
+    # the replay in the tracker's own item shape (6 tiles x 16 particles since round 2; earlier lines: 4 tiles)
+    rep = [x for x in load_jsonl("r02_gather_replay.jsonl")
+           if x.get("init_noise_deg_cm") == 5.0 and x.get("frame") == 12 and x.get("tiles", 4) == 6]
     gather_view = None
     if rep:
         x = rep[0]
         gather_view = {"replay_evals_per_s": x["replay_evals_per_s"], "frac": kernel_evals_s / x["replay_evals_per_s"],
                        "inband_frac": x["inband_frac"],
                        "source": "profiles/r02_gather_replay.jsonl: the evaluation's exact mask + record address "
-                                 "stream of a bench frame replayed without arithmetic (frame 12, +-5 deg/cm init)"}
+                                 "stream of a bench frame replayed without arithmetic in the tracker's item order "
+                                 "(6-tile x 16-particle warp items; frame 12, +-5 deg/cm init)"}
     roofline = {"bound": "gather", "achieved": gather_gbs, "peak": gather_peak, "unit": "GB/s",
                 "frac": gather_gbs / gather_peak if gather_peak else None, "traffic": traffic, "kernel": kname,
                 "basis": f"{BYTES_PER_EVAL} B cell record gathered per particle-point evaluation (the record holds the "

@@ -31,6 +31,9 @@ def rodrigues(r):
     return np.eye(3) + np.sin(th) / th * K + (1.0 - np.cos(th)) / th ** 2 * (K @ K)
 
 
+TILES = int(os.environ.get("REPLAY_TILES", "6"))  # the tracker's item width (points per lane)
+
+
 def main():
     dev = torch.device("cuda", 0)
     seq = Sequence("Q", seed=1, n_frames=16, K=2048, iters=10)
@@ -125,12 +128,12 @@ def main():
         ms = C.c_float()
         rc = lib.replay_run(C.c_void_p(idx_d.data_ptr()), K, npad, C.c_void_p(rec.data_ptr()),
                             C.c_void_p(mask.data_ptr()), 5, C.c_void_p(queue.data_ptr()), C.c_void_p(out.data_ptr()),
-                            C.byref(ms))
+                            C.byref(ms), TILES)
         assert rc == 0, rc
         replay_ms += ms.value
         del idx_d
     evals = K * n_valid * seq.params.iters
-    res = {"tool": "gather_replay", "frame": t, "init_noise_deg_cm": noise, "K": K, "npad": npad, "n_valid": n_valid, "iters": seq.params.iters,
+    res = {"tool": "gather_replay", "tiles": TILES, "frame": t, "init_noise_deg_cm": noise, "K": K, "npad": npad, "n_valid": n_valid, "iters": seq.params.iters,
            "inband_frac": n_inb / (K * npad * seq.params.iters),
            "replay_ms": replay_ms, "replay_evals_per_s": evals / (replay_ms * 1e-3),
            "index_stream_bytes_per_iter": K * npad * 4,

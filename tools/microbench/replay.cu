@@ -1,7 +1,7 @@
 // Gather-replay ceiling (SURVEY.md §8(d-3) roofline denominator (4)): replays the evaluation's
 // exact address stream -- per (particle, point) the cell's in-band mask word and then its 32-byte
-// record (record 0 when out of band), in the tracker's work-item order (4 tiles x 16 particles per
-// warp item from one dynamic queue, 4 points per lane batched) -- with no transform and no lerp.
+// record (record 0 when out of band), in the tracker's work-item order (TILES tiles x 16 particles per
+// warp item from one dynamic queue, TILES points per lane batched; the tracker uses 6 since round 2) -- with no transform and no lerp.
 // The packed index stream (bit 31 in-band, bits 0..30 the record index) is precomputed on the host
 // by tools/gather_replay.py and streamed with evict-first loads (157 MB per iteration at config Q),
 // prefetched two particles ahead so that its HBM latency is not part of the replayed chain (r01
@@ -18,11 +18,12 @@ __device__ __forceinline__ void ld32(const float* p, float (&v)[8]) {
                : "l"(p));
 }
 
+template <int TILES>
 __global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ idx, int K, int npad,
                                                    const float* __restrict__ rec, const unsigned* __restrict__ mask,
                                                    unsigned* __restrict__ queue, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int ngroups = npad / 128, nch = (K + 15) / 16;
+  const int ngroups = (npad + 32 * TILES - 1) / (32 * TILES), nch = (K + 15) / 16;
   const int nitems = ngroups * nch;
   float acc = 0.f;
   for (;;) {
@@ -34,22 +35,25 @@ __global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ 
     const int k0 = chunk * 16, k1 = min(K, k0 + 16);
     // the index stream is prefetched two particles ahead (registers), so its HBM latency is off the
     // replayed chain: what remains is the tracker's own dependent pair, mask word -> record
-    const uint32_t* base = idx + (group * 4) * 32 + lane;
-    uint32_t wn[2][4];
+    const uint32_t* base = idx + (group * TILES) * 32 + lane;
+    bool in[TILES];  // slots beyond npad (the last group) replay as out of range (index word 0)
+#pragma unroll
+    for (int p = 0; p < TILES; ++p) in[p] = (group * TILES + p) * 32 + lane < npad;
+    uint32_t wn[2][TILES];
 #pragma unroll
     for (int d = 0; d < 2; ++d)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) wn[d][p] = k0 + d < k1 ? __ldcs(base + (size_t)(k0 + d) * npad + p * 32) : 0u;
+      for (int p = 0; p < TILES; ++p) wn[d][p] = k0 + d < k1 && in[p] ? __ldcs(base + (size_t)(k0 + d) * npad + p * 32) : 0u;
     for (int k = k0; k < k1; ++k) {
-      uint32_t w[4], mw[4];
+      uint32_t w[TILES], mw[TILES];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) { w[p] = wn[0][p]; wn[0][p] = wn[1][p]; }
+      for (int p = 0; p < TILES; ++p) { w[p] = wn[0][p]; wn[0][p] = wn[1][p]; }
 #pragma unroll
-      for (int p = 0; p < 4; ++p) wn[1][p] = k + 2 < k1 ? __ldcs(base + (size_t)(k + 2) * npad + p * 32) : 0u;
+      for (int p = 0; p < TILES; ++p) wn[1][p] = k + 2 < k1 && in[p] ? __ldcs(base + (size_t)(k + 2) * npad + p * 32) : 0u;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) mw[p] = __ldg(mask + ((w[p] & 0x7fffffffu) >> 5));
+      for (int p = 0; p < TILES; ++p) mw[p] = __ldg(mask + ((w[p] & 0x7fffffffu) >> 5));
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
+      for (int p = 0; p < TILES; ++p) {
         const uint32_t o = w[p] & 0x7fffffffu;
         const uint32_t inb = (w[p] >> 31) & (mw[p] >> (o & 31u));  // the mask is all ones: inb, with the dependency
         float v[8];
@@ -63,7 +67,7 @@ __global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ 
 }  // namespace
 
 extern "C" int replay_run(const uint32_t* idx, int K, int npad, const float* rec, const unsigned* mask, int reps,
-                          unsigned* queue, float* out, float* ms_out) {
+                          unsigned* queue, float* out, float* ms_out, int tiles) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -71,7 +75,8 @@ extern "C" int replay_run(const uint32_t* idx, int K, int npad, const float* rec
   for (int r = 0; r < reps + 1; ++r) {
     cudaMemset(queue, 0, 4);
     cudaEventRecord(e0);
-    k_replay<<<296, 256>>>(idx, K, npad, rec, mask, queue, out);
+    if (tiles == 6) k_replay<6><<<296, 256>>>(idx, K, npad, rec, mask, queue, out);
+    else k_replay<4><<<296, 256>>>(idx, K, npad, rec, mask, queue, out);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0.f;
