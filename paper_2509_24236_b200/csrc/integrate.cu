@@ -292,9 +292,19 @@ __device__ __forceinline__ int box_class(const Geom& g, const Intr& K, const dou
   const float y = (float)Tdev[1] * cwx + (float)Tdev[5] * cwy + (float)Tdev[9] * cwz;
   const float z = (float)Tdev[2] * cwx + (float)Tdev[6] * cwy + (float)Tdev[10] * cwz;
   if (!(z + rad > 0.f)) return kCull;
-  if (z - rad <= 1e-3f) return kKeep;  // straddles the camera plane: no projection bound
-  const float zn = z - rad, zf = z + rad;
   const float fx = (float)K.fx, fy = (float)K.fy, cx = (float)K.cx, cy = (float)K.cy;
+  if (z - rad <= 1e-3f) {
+    // straddles the camera plane: no projection bound, but the frustum there is a thin cone from
+    // the camera centre.  A voxel (xv, yv, zv), zv > 0, lands on a pixel only if |xv| <= zv * ax
+    // (ax = the larger half-width of the image in pixels / fx, +1/2 pixel for the rounding) and
+    // |yv| <= zv * ay; every voxel here has zv <= z + rad and |xv| >= |x| - rad, so a box laterally
+    // beyond the cone at its far depth cannot be updated (1% + 1 mm of slack for the fp32 transform)
+    const float zf = z + rad;
+    const float ax = fmaxf(cx + 0.5f, (float)K.W - 0.5f - cx) / fx, ay = fmaxf(cy + 0.5f, (float)K.H - 0.5f - cy) / fy;
+    if (fabsf(x) - rad > 1.01f * zf * ax + 1e-3f || fabsf(y) - rad > 1.01f * zf * ay + 1e-3f) return kCull;
+    return kKeep;
+  }
+  const float zn = z - rad, zf = z + rad;
   const float izn = __frcp_rn(zn), izf = __frcp_rn(zf);  // (a few ulp: far inside the 2 px margin)
   const float u0 = fx * fminf((x - rad) * izn, (x - rad) * izf) + cx - 2.f;
   const float u1 = fx * fmaxf((x + rad) * izn, (x + rad) * izf) + cx + 2.f;
