@@ -1188,7 +1188,10 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long gen = 0ull;  // grid-barrier arrival target
   // PFT_PHASE_TIMING accumulators (CTA 0, thread 0): B, P1, P2, P3, P4, P5, P2 tail, P0
-  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tmark = 0;
+  // (zero-initialised from a value ptxas cannot fold, a.K >= 1: a constant 0 was materialised
+  // with 'CS2R Rx, SRZ' and spilled 5 cycles later, the idiom of DESIGN.md §9)
+  const unsigned long long z0 = (unsigned long long)(a.K < 0);
+  unsigned long long tph[8] = {z0, z0, z0, z0, z0, z0, z0, z0}, tmark = z0;
   const bool timing = a.tdone != nullptr;
   if (timing && tid == 0) tmark = global_ns();
   __shared__ unsigned long long sXround;

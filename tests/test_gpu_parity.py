@@ -342,6 +342,36 @@ def test_integrate_room_bit_exact(pft, storage):
     vol_full.close()
 
 
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_integrate_camera_plane_cone(pft, storage):
+    """The cull of boxes straddling the camera plane (integrate.cu box_class: culled only when
+    laterally outside the frustum cone at their far depth): the camera sits inside a 64^3 @ 1 cm
+    volume, rotated off the grid axes, facing a surface 3-20 cm away, so voxels with 0 < z < 20 cm
+    near the optical axis are updated while their bricks straddle z = 0.  Culled path and full sweep
+    against the oracle bit for bit, and the culled path's updated-voxel count equals the oracle's."""
+    desc = VolumeDesc(64, 64, 64, 0.01, (-0.32, -0.32, -0.32), 0.03, storage=storage)
+    intr = Intrinsics(80.0, 80.0, 39.5, 29.5, 80, 60)
+    T0 = perturb(np.hstack([np.eye(3), np.zeros((3, 1))]), [0.3, -0.2, 0.1], [0.3, -0.2, 0.1], 25.0, 0.5)
+    v, u = np.mgrid[0:60, 0:80]
+    depth = (30 + (u + 2 * v) % 171).astype(np.uint16)  # 3 .. 20 cm, a ramp with steps
+    depth[::7, ::5] = 0                                  # scattered invalid pixels
+    vol = gpu_volume(pft, desc)
+    vfull = gpu_volume(pft, desc)
+    ov = oracle.OracleVolume(desc)
+    for f in range(2):
+        vol.integrate(T(depth), intr, T(T0))
+        vfull.integrate(T(depth), intr, T(T0), full_sweep=True)
+        n_ora = ov.integrate(depth, intr, T0)
+        assert vol.integrate_stats()["updated_voxels"] == n_ora > 100
+    for v_ in (vol, vfull):
+        V, W = [x.cpu().numpy() for x in v_.download()]
+        assert np.array_equal(storage_bits(V), storage_bits(ov.V)), \
+            f"{int((storage_bits(V) != storage_bits(ov.V)).sum())} voxel values differ"
+        assert np.array_equal(storage_bits(W), storage_bits(ov.W))
+    vol.close()
+    vfull.close()
+
+
 @pytest.mark.parametrize("voxel", [0.0625, 0.05])
 @pytest.mark.parametrize("storage", ["f32", "f16"])
 def test_integrate_grid_aligned_pixel_ties(pft, voxel, storage):
