@@ -244,7 +244,7 @@ __device__ __forceinline__ void bitonic256(unsigned long long* key, int* idx, in
   for (int k = 2; k <= 256; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       const int p = tid ^ j;
-      if (p > tid) {
+      if (tid < 256 && p > tid) {
         const bool up = (tid & k) == 0;
         const bool gt = key_less(key[p], idx[p], key[tid], idx[tid]);
         if (up == gt) {
@@ -259,8 +259,10 @@ __device__ __forceinline__ void bitonic256(unsigned long long* key, int* idx, in
 // One 256-particle block's top-k candidates: sorted (key, index) of its members, padded with ~0.
 __device__ __forceinline__ void block_topk(unsigned long long key_mine, int k, int topk, unsigned long long* skey,
                                            int* sidx, unsigned long long* cand_key, int* cand_idx, int tid) {
-  skey[tid] = key_mine;
-  sidx[tid] = k;
+  if (tid < 256) {
+    skey[tid] = key_mine;
+    sidx[tid] = k;
+  }
   bitonic256(skey, sidx, tid);
   if (tid < topk) { cand_key[tid] = skey[tid]; cand_idx[tid] = sidx[tid]; }
   __syncthreads();
@@ -283,8 +285,10 @@ __device__ __noinline__ void topk_finish(const unsigned long long* cand_key, con
         kk = __ldcg(cand_key + b * kTopkMax + head);
         ii = __ldcg(cand_idx + b * kTopkMax + head);
       }
-    skey[tid] = kk;
-    sidx[tid] = ii;
+    if (tid < 256) {
+      skey[tid] = kk;
+      sidx[tid] = ii;
+    }
     __syncthreads();
     for (int s = 128; s > 0; s >>= 1) {
       if (tid < s && key_less(skey[tid + s], sidx[tid + s], skey[tid], sidx[tid])) {
@@ -1004,6 +1008,21 @@ constexpr int kItemTiles = PFT_ITEM_TILES;  // 8x4 tiles per warp item (= points
 #define PFT_ITEM_PARTICLES 16
 #endif
 constexpr int kItemParticles = PFT_ITEM_PARTICLES;
+// CTA size of the persistent tracker: 512 threads at 1 CTA/SM (16 warps, 128 registers each, the
+// same warps per SM as 2 x 256) halves the CTAs that take part in every grid barrier and serial phase
+#ifndef PFT_PERSIST_THREADS
+#define PFT_PERSIST_THREADS 256
+#endif
+constexpr int kPT = PFT_PERSIST_THREADS;
+static_assert(kPT % 256 == 0, "update blocks are 256 particles");
+// dynamic shared memory: red (update phases) and sPart (evaluation phase) are never live at the
+// same time (the union), then the warps' pose slots
+constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
+constexpr size_t kTopBytes = 256 * (sizeof(unsigned long long) + sizeof(int));
+constexpr size_t kPartBytes = (kPT / 32) * kItemParticles * 33 * sizeof(unsigned long long);
+constexpr size_t kUnionBytes = kPartBytes > kRedBytes + kTopBytes ? kPartBytes : kRedBytes + kTopBytes;
+constexpr size_t kWPoseBytes = (kPT / 32) * kItemParticles * 6 * sizeof(double2);
+constexpr size_t kPersistDynSmem = kUnionBytes + kWPoseBytes;
 
 struct PArgs {
   const void* R;
@@ -1086,14 +1105,14 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
   __syncthreads();
 }
 
-template <typename T>
+template <typename T, int NT>
 __device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsigned long long* __restrict__ mask,
                                              const Geom& g, const Points& pts, const double* m, int flag,
                                              int nb, int lb, unsigned long long& sum, unsigned& cnt,
                                              const double* pre = nullptr) {
   const int per = (pts.npad + nb - 1) / nb;
   const int b0 = lb * per, b1 = min(pts.npad, b0 + per);
-  for (int base = b0; base < b1; base += kThreads) {
+  for (int base = b0; base < b1; base += NT) {
     const int i = base + threadIdx.x;
     double px[1] = {0.0}, py[1] = {0.0}, pz[1] = {0.0};
     if (pre && base == b0) { px[0] = pre[0]; py[0] = pre[1]; pz[0] = pre[2]; }  // first pass, loaded early
@@ -1106,24 +1125,8 @@ __device__ __forceinline__ void centre_slice(const T* __restrict__ V, const unsi
   }
 }
 
-// Sum of the G per-CTA centre partials (S, n), read by all threads (2 loads each) and reduced by
-// warp shuffles + smem: the same exact integers in every CTA, ~L2 latency instead of G of them.
-__device__ __forceinline__ void sum_partials(const unsigned long long* cp, int G, unsigned long long* sS,
-                                             unsigned* sN, unsigned long long& S, unsigned long long& n) {
-  unsigned long long s = 0ull, c = 0ull;
-  for (int b = threadIdx.x; b < G; b += kThreads) { s += __ldcg(cp + 2 * b); c += __ldcg(cp + 2 * b + 1); }
-  for (int sft = 16; sft > 0; sft >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, sft);
-    c += __shfl_xor_sync(0xffffffffu, c, sft);
-  }
-  if ((threadIdx.x & 31) == 0) { sS[threadIdx.x >> 5] = s; sN[threadIdx.x >> 5] = (unsigned)c; }
-  __syncthreads();
-  S = 0ull; n = 0ull;
-  for (int w = 0; w < kThreads / 32; ++w) { S += sS[w]; n += sN[w]; }
-  __syncthreads();
-}
-
-// CTA total of the centre's (sum, cnt) -> thread 0.
+// CTA total of the centre's (sum, cnt) -> thread 0 (NT threads).
+template <int NT>
 __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt, unsigned long long* sS, unsigned* sN,
                                             unsigned long long& S, unsigned& n) {
   unsigned long long ws;
@@ -1133,29 +1136,25 @@ __device__ __forceinline__ void block_total(unsigned long long sum, unsigned cnt
   __syncthreads();
   S = 0ull; n = 0u;
   if (threadIdx.x == 0)
-    for (int w = 0; w < kThreads / 32; ++w) { S += sS[w]; n += sN[w]; }
+    for (int w = 0; w < NT / 32; ++w) { S += sS[w]; n += sN[w]; }
   __syncthreads();
 }
 
 template <typename T>
 #ifndef PFT_PERSIST_MINB
-#define PFT_PERSIST_MINB 2
+#define PFT_PERSIST_MINB (512 / PFT_PERSIST_THREADS)
 #endif
-__global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent(PArgs a) {
-  // red (update phases) and sPart (evaluation phase) are never live at the same time
-  constexpr size_t kRedBytes = kUpdW * 256 * sizeof(double);
-  constexpr size_t kTopBytes = 256 * (sizeof(unsigned long long) + sizeof(int));
-  constexpr size_t kPartBytes = (kThreads / 32) * kItemParticles * 33 * sizeof(unsigned long long);
-  constexpr size_t kUnionBytes = kPartBytes > kRedBytes + kTopBytes ? kPartBytes : kRedBytes + kTopBytes;
-  __shared__ __align__(16) unsigned char sUnion[kUnionBytes];
+__global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArgs a) {
+  extern __shared__ __align__(16) unsigned char sDyn[];
+  unsigned char* const sUnion = sDyn;
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12], sPprev[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
   __shared__ int sFlagC, sNA, sItem, sStalls, sStop, sSet, sKlast, sRej;
   __shared__ unsigned sNc, sNcBase;
-  __shared__ unsigned long long sS[kThreads / 32];
-  __shared__ unsigned sNw[kThreads / 32];
-  __shared__ double2 sWPose[kThreads / 32][kItemParticles * 6];
+  __shared__ unsigned long long sS[kPT / 32];
+  __shared__ unsigned sNw[kPT / 32];
+  double2 (*sWPose)[kItemParticles * 6] = reinterpret_cast<double2 (*)[kItemParticles * 6]>(sDyn + kUnionBytes);
   __shared__ int sTopSel[kTopkMax];
   // per-lane partials of the item's particles: (fix | cnt << 32), rows padded against bank conflicts
   unsigned long long (*sPart)[kItemParticles][33] =
@@ -1187,6 +1186,11 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
   const int kloc = (a.K + G - 1) / G, kb = grp * kloc;            // shard: rows [kb, kb + kloc)
   const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long gen = 0ull;  // grid-barrier arrival target
+  // centre sums: every CTA adds its (S, n) into slot cev % 3 of a 3-slot ring (exact integers, any
+  // order); CTA 0 zeroes slot (cev + 1) % 3 during evaluation cev -- its last readers (evaluation
+  // cev - 2) all passed the barrier of evaluation cev - 1 -- and the barrier of evaluation cev orders
+  // that store before evaluation cev + 1's atomics.  Slot 0 is zeroed in P0.
+  int cev = 0;
   // PFT_PHASE_TIMING accumulators (CTA 0, thread 0): B, P1, P2, P3, P4, P5, P2 tail, P0
   // (zero-initialised from a value ptxas cannot fold, a.K >= 1: a constant 0 was materialised
   // with 'CS2R Rx, SRZ' and spilled 5 cycles later, the idiom of DESIGN.md §9)
@@ -1217,11 +1221,11 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
   const unsigned long long xround0 = sXround;
   // ---- P0: points of every set (a1/a2), accumulators, pmax
   {
-    const int stride = nb * kThreads;
+    const int stride = nb * kPT;
     double pm = 0.0;
     for (int sidx = 0; sidx < nsets; ++sidx) {
       const PSet ps = sSets[sidx];
-      for (int i0 = lb * kThreads; i0 < ps.npad; i0 += stride) {
+      for (int i0 = lb * kPT; i0 < ps.npad; i0 += stride) {
         const int i = i0 + tid;  // npad is a multiple of 32: whole warps stay converged
         double X = 0.0, Y = 0.0, Z = 0.0;
         bool valid = false;
@@ -1236,7 +1240,8 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     }
     for (int sft = 16; sft > 0; sft >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, sft));
     if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
-    for (int k = lb * kThreads + tid; k < kloc; k += stride) { acc[k].S = 0ull; acc[k].n = 0u; }
+    for (int k = lb * kPT + tid; k < kloc; k += stride) { acc[k].S = 0ull; acc[k].n = 0u; }
+    if (lb == 0 && tid == 0) { cpart[0] = 0ull; cpart[1] = 0ull; }
   }
   if (tid == 0) {
     for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
@@ -1265,15 +1270,20 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
       __syncthreads();
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
+      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
       unsigned long long S;
       unsigned n;
-      block_total(sum, cnt, sS, sNw, S, n);
-      // half 0 of the centre partials: P5 of the previous iteration may still be reading half 1
-      if (tid == 0) { cpart[2 * lb] = S; cpart[2 * lb + 1] = n; }
+      block_total<kPT>(sum, cnt, sS, sNw, S, n);
+      unsigned long long* slot = cpart + 2 * (cev % 3);
+      if (tid == 0) {
+        if (lb == 0) { cpart[2 * ((cev + 1) % 3)] = 0ull; cpart[2 * ((cev + 1) % 3) + 1] = 0ull; }
+        atomicAdd(slot, S);
+        atomicAdd(slot + 1, (unsigned long long)n);
+      }
       grid_barrier(st, gen, nb, a.watchdog_ns);
-      unsigned long long S2, n2;
-      sum_partials(cpart, nb, sS, sNw, S2, n2);
+      ++cev;
+      unsigned long long S2 = 0ull, n2 = 0ull;
+      if (tid == 0) { S2 = __ldcg(slot); n2 = __ldcg(slot + 1); }
       if (tid == 0) {
         sState[2] = fitness_c(S2, (unsigned)n2, a.rho, N);
         sNc = (unsigned)n2;
@@ -1285,7 +1295,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     // ---- P1: candidate-pose table (K_i rows), interleaved over all CTAs (row kb + tid*nb + lb):
     // each pose is a ~2500-cycle fp64 chain, so K = 2048 rows on 296 CTAs x ~7 threads is one
     // chain's latency, where contiguous 256-row slices put them all on 8 SMs' fp64 pipes
-    for (int k = kb + tid * nb + lb; k < min(Ki, kb + kloc); k += nb * kThreads) {
+    for (int k = kb + tid * nb + lb; k < min(Ki, kb + kloc); k += nb * kPT) {
       double m[12];
       pflag[k] = candidate_pose(a.pst + 6 * (size_t)k, sState[0], sState[1], sP, a.conv, a.g, pmax, m);
       double2* row = (double2*)(ptab + 12 * (size_t)k);
@@ -1297,7 +1307,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     // blocks' few SMs
 #ifdef PFT_MEMBER_TABLE
     if (a.rule != 2)
-      for (int k = (kThreads - 1 - tid) * nb + lb; k < Ki; k += nb * kThreads) {
+      for (int k = (kPT - 1 - tid) * nb + lb; k < Ki; k += nb * kPT) {
         double q[4], u[3];
         member_delta(a.pst + 6 * (size_t)k, sState[0], sState[1], q, u);
         double2* mrow = (double2*)(mtab + 8 * (size_t)k);
@@ -1320,7 +1330,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
       const int ngroups = (pts.npad + 32 * kItemTiles - 1) / (32 * kItemTiles);
       const int nch16 = (Ks + kItemParticles - 1) / kItemParticles;
       // (only when there are few items per warp: with many, the tail is already negligible)
-      const bool few = (long long)ngroups * nch16 < 64LL * nb * (kThreads / 32);
+      const bool few = (long long)ngroups * nch16 < 64LL * nb * (kPT / 32);
       const int cb = (a.sched == 1 || !few) ? nch16 : nch16 - (nch16 * a.tail_pct + 99) / 100;  // big chunks
       const int ksmall = cb * kItemParticles;                           // first particle of the small part
       const int nch4 = (Ks - ksmall + 3) / 4;
@@ -1429,7 +1439,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     const PartRec* recs = acc;
     if (G > 1) {
       const size_t half = (size_t)((xround0 + (unsigned long long)it) & 1ull) * a.xhalf;  // global round parity
-      for (int j = lb * kThreads + tid; j < Ks; j += nb * kThreads) {
+      for (int j = lb * kPT + tid; j < Ks; j += nb * kPT) {
         const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2*>(acc + j));  // (S, n | pad)
         for (int q = 0; q < G; ++q) __stcg(reinterpret_cast<ulonglong2*>((PartRec*)sXbuf[q] + half + kb + j), r);
         acc[j].S = 0ull;
@@ -1464,7 +1474,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     unsigned long long* tkey = reinterpret_cast<unsigned long long*>(sUnion + kRedBytes);  // top-k scratch
     int* tidx = reinterpret_cast<int*>(sUnion + kRedBytes + 256 * sizeof(unsigned long long));
     for (int b = lb; b < nblk; b += nb) {
-      const int k = b * 256 + tid;
+      const int k = tid < 256 ? b * 256 + tid : Ki;  // (threads >= 256 of a 512-thread CTA idle)
       double row[kUpdW];
 #pragma unroll
       for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
@@ -1494,8 +1504,9 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
       if (a.rule == 2) {
         block_topk(key, k, a.topk, tkey, tidx, ckey + (size_t)b * kTopkMax, cidx + (size_t)b * kTopkMax, tid);
       } else {
+        if (tid < 256)
 #pragma unroll
-        for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
+          for (int c = 0; c < kUpdW; ++c) red[c][tid] = row[c];
         treeW(red, tid);
         if (tid < kUpdW) upart[b * kUpdW + tid] = red[tid][0];
         __syncthreads();
@@ -1519,11 +1530,13 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
       if (tid == 8) red[8][0] = __ldcg(tkout + 7);  // weight sum = number selected
       __syncthreads();
     } else {
+      if (tid < 256) {
 #pragma unroll
-      for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
-      for (int b = tid; b < nblk; b += 256)
+        for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
+        for (int b = tid; b < nblk; b += 256)
 #pragma unroll
-        for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(upart + b * kUpdW + c);
+          for (int c = 0; c < kUpdW; ++c) red[c][tid] += __ldcg(upart + b * kUpdW + c);
+      }
       treeW(red, tid);
     }
     if (tid == 0) {
@@ -1545,19 +1558,24 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt, cpre);
+      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt, cpre);
       unsigned long long S;
       unsigned n;
-      block_total(sum, cnt, sS, sNw, S, n);
-      // half 1 of the centre partials (read in P5 below; the next baseline B writes half 0)
-      unsigned long long* cp1 = cpart + 2 * (size_t)nb;
-      if (tid == 0) { cp1[2 * lb] = S; cp1[2 * lb + 1] = n; }
+      block_total<kPT>(sum, cnt, sS, sNw, S, n);
+      if (tid == 0) {
+        if (lb == 0) { cpart[2 * ((cev + 1) % 3)] = 0ull; cpart[2 * ((cev + 1) % 3) + 1] = 0ull; }
+        atomicAdd(cpart + 2 * (cev % 3), S);
+        atomicAdd(cpart + 2 * (cev % 3) + 1, (unsigned long long)n);
+      }
       grid_barrier(st, gen, nb, a.watchdog_ns);  // sNA is identical in every CTA: uniform barrier
     }
     PFT_TMARK(4);
     // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
     unsigned long long S5 = 0ull, n5 = 0ull;
-    if (sNA > 0) sum_partials(cpart + 2 * (size_t)nb, nb, sS, sNw, S5, n5);
+    if (sNA > 0) {
+      if (tid == 0) { S5 = __ldcg(cpart + 2 * (cev % 3)); n5 = __ldcg(cpart + 2 * (cev % 3) + 1); }
+      ++cev;
+    }
     if (tid == 0) {
       double Ec = sState[3];
       unsigned nc = sNcBase;
@@ -1610,7 +1628,7 @@ __global__ __launch_bounds__(kThreads, PFT_PERSIST_MINB) void k_track_persistent
     }
   }
   if (out_rank)
-    for (int k = sKlast + lb * kThreads + tid; k < a.K; k += nb * kThreads) {
+    for (int k = sKlast + lb * kPT + tid; k < a.K; k += nb * kPT) {
       a.E_out[k] = 1.0;
       a.n_out[k] = 0;
     }
@@ -1672,7 +1690,7 @@ pft_status track_layout(const pft_volume* vol, const pft_intrinsics* K, int32_t 
   L->part_off = off; off = align_up(off + kUpdW * sizeof(double) * (size_t)L->nblk_upd, 256);
   L->ptab_off = off; off = align_up(off + (12 * sizeof(double) + sizeof(int)) * (size_t)nparticles, 256);
   L->mtab_off = off; off = align_up(off + 8 * sizeof(double) * (size_t)nparticles, 256);
-  L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // two halves
+  L->cpart_off = off; off = align_up(off + 2 * 2 * sizeof(unsigned long long) * 148 * 8, 256);  // centre-sum ring (3 x (S, n))
   L->work_off = off; off = align_up(off + sizeof(unsigned) * 1024 + sizeof(unsigned long long) * 148 * 8, 256);
   L->topk_off = off;
   off = align_up(off + (sizeof(unsigned long long) + sizeof(int)) * kTopkMax * (size_t)L->nblk_upd + 16 * sizeof(double), 256);
@@ -1813,11 +1831,13 @@ static int persistent_cap() {
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     if (cudaFuncGetAttributes(&fa, k_track_persistent<T>) == cudaSuccess && smem_sm > 0)
-      carve = (int)((200.0 * ((double)fa.sharedSizeBytes + 1024.0) + smem_sm - 1) / smem_sm);
+      carve = (int)((100.0 * PFT_PERSIST_MINB * ((double)fa.sharedSizeBytes + (double)kPersistDynSmem + 1024.0) + smem_sm - 1) /
+                    smem_sm);
   }
+  cudaFuncSetAttribute(k_track_persistent<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPersistDynSmem);
   if (carve >= 0 && carve <= 100)
     cudaFuncSetAttribute(k_track_persistent<T>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track_persistent<T>, kPT, kPersistDynSmem);
   cap = per_sm * sms;
   if (cap > 148 * 8) cap = 148 * 8;
   if (cap < 1) cap = -1;
@@ -1919,7 +1939,8 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   void* args[] = {&pa};
   cudaError_t e = cudaSuccess;
   PFT_LAUNCH(PFT_PROF_TRACK, c.st,
-             e = cudaLaunchCooperativeKernel((const void*)k_track_persistent<T>, dim3(grid), dim3(kThreads), args, 0, c.st));
+             e = cudaLaunchCooperativeKernel((const void*)k_track_persistent<T>, dim3(grid), dim3(kPT), args,
+                                             kPersistDynSmem, c.st));
   if (e == cudaErrorCooperativeLaunchTooLarge && G == 1 && !emul) {
     cudaGetLastError();  // not sticky: the SMs are partly taken (e.g. by another context)
     return PFT_ERR_UNSUPPORTED;  // the caller falls back to the multi-launch tracker

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Interleaved A/B of library builds on the bench (no ncu), ROUNDS rounds.  usage: tools/ab2.sh ROUNDS lib_a.so lib_b.so ...
+R=$1; shift
+for r in $(seq 1 $R); do
+  for lib in "$@"; do
+    label=$(basename $lib .so)_$r
+    PFT_LIB=$lib python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-large > gpurun_out/ab_$label.json 2> gpurun_out/ab_$label.err
+    python -c "
+import json; d=json.load(open('gpurun_out/ab_$label.json')); print('$label', round(d['value']/1e9,2), 'Gevals/s', round(d['ms_per_step'],4), 'ms/frame', {k:round(v,4) for k,v in d['kernel_ms_per_step'].items()}, 'eval', round(d['roofline']['evals_per_s_kernel']/1e9,1), 'agree', d.get('runs_agree'))" || tail -3 gpurun_out/ab_$label.err
+  done
+done
