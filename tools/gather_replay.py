@@ -8,7 +8,9 @@ camera-centred); computes on the host, in fp64, every (particle, point) cell and
 centre equals the tracker's n_c).  tools/microbench/libreplay.so
 then replays exactly those mask-word and record loads on the GPU in the tracker's item order,
 without the transform or the lerp.  Prints one JSON line: the replay's evaluations/s (the gather
-ceiling for this access pattern) next to the tracker's."""
+ceiling for this access pattern) next to the tracker's.  A second replay generates the same
+stream on the device (fp32 cells from fp32 folded poses, the real in-band mask: no 157 MB/iteration
+index stream from HBM); the ceiling is the faster of the two."""
 import ctypes as C
 import json
 import os
@@ -98,6 +100,17 @@ def main():
     out = torch.zeros(296, dtype=torch.float32, device=dev)
     lib = C.CDLL(os.path.join(ROOT, "tools", "microbench", "libreplay.so"))
     replay_ms, n_inb = 0.0, 0
+    # device-generated replay (no index stream): the REAL in-band mask in brick-order bits, fp32
+    # points (invalid slots z = 0) and per-iteration fp32 folded poses
+    zc, yc, xc = np.nonzero(inb)
+    bit = (((xc >> 2) << 6) | (xc & 3)) + (yc >> 2) * sy + ((yc & 3) << 2) + (zc >> 2) * sz + ((zc & 3) << 4)
+    words = np.zeros(nrec // 32 + 1, dtype=np.uint32)
+    np.bitwise_or.at(words, bit >> 5, (np.uint32(1) << (bit & 31).astype(np.uint32)))
+    real_mask = torch.from_numpy(words.view(np.int32)).to(dev)
+    del zc, yc, xc, bit, words
+    pts32 = torch.from_numpy(np.where(ok[None, :], P, 0.0).astype(np.float32).copy()).to(dev)
+    out_gen = torch.zeros(1 + 296, dtype=torch.int64, device=dev)
+    gen_ms, gen_inb = 0.0, 0
     n_valid = int(ok.sum())
     # sanity: the in-band count of the final centre pose, host-computed, against the tracker's n_c
     Pf = trace[seq.params.iters - 1, 4:16].reshape(3, 4)
@@ -111,10 +124,12 @@ def main():
         Pc = T0 if it == 0 else trace[it - 1, 4:16].reshape(3, 4)
         om, vv = trace[it, 2], trace[it, 3]
         idx = np.zeros((K, npad), dtype=np.uint32)
+        fold = np.zeros((K, 12), dtype=np.float64)
         for k in range(K):
             dR = rodrigues(pst[k, :3] * om * np.pi / 180.0)
             R = dR @ Pc[:, :3]
             tk = Pc[:, 3] + pst[k, 3:] * vv / 100.0
+            fold[k] = np.concatenate([R / d.voxel_m, ((tk - o) / d.voxel_m - 0.5)[:, None]], axis=1).reshape(12)
             g = (R @ P + (tk - o)[:, None]) / d.voxel_m - 0.5
             cl = np.floor(g).astype(np.int64)
             valid = ok & (cl[0] >= 0) & (cl[0] <= nx - 2) & (cl[1] >= 0) & (cl[1] <= ny - 2) & (cl[2] >= 0) & (cl[2] <= nz - 2)
@@ -132,13 +147,23 @@ def main():
         assert rc == 0, rc
         replay_ms += ms.value
         del idx_d
+        poses_d = torch.from_numpy(fold.astype(np.float32)).to(dev)
+        rc = lib.replay_gen_run(C.c_void_p(poses_d.data_ptr()), C.c_void_p(pts32.data_ptr()), K, npad, nx, ny, nz,
+                                C.c_uint(sy), C.c_uint(sz), C.c_void_p(rec.data_ptr()), C.c_void_p(real_mask.data_ptr()), 5,
+                                C.c_void_p(queue.data_ptr()), C.c_void_p(out_gen.data_ptr()), C.byref(ms), TILES)
+        assert rc == 0, rc
+        gen_ms += ms.value
+        gen_inb += int(out_gen[0].item())
     evals = K * n_valid * seq.params.iters
     res = {"tool": "gather_replay", "tiles": TILES, "frame": t, "init_noise_deg_cm": noise, "K": K, "npad": npad, "n_valid": n_valid, "iters": seq.params.iters,
            "inband_frac": n_inb / (K * npad * seq.params.iters),
            "replay_ms": replay_ms, "replay_evals_per_s": evals / (replay_ms * 1e-3),
            "index_stream_bytes_per_iter": K * npad * 4,
            "track_ms": track_ms, "track_evals_per_s": evals / (track_ms * 1e-3),
-           "track_over_replay": replay_ms / track_ms}
+           "track_over_replay": replay_ms / track_ms,
+           "gen_replay_ms": gen_ms, "gen_replay_evals_per_s": evals / (gen_ms * 1e-3),
+           "gen_inband_evals": gen_inb, "host_inband_evals": n_inb,
+           "ceiling_evals_per_s": evals / (min(replay_ms, gen_ms) * 1e-3)}
     print(json.dumps(res))
 
 

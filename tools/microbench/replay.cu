@@ -64,7 +64,95 @@ __global__ __launch_bounds__(256, 2) void k_replay(const uint32_t* __restrict__ 
   }
   if (acc == 1234.5f) out[blockIdx.x] = acc;
 }
+// Device-generated variant (no index stream): the candidate poses of one iteration as fp32 3x4
+// grid-coordinate transforms g = M p + c (folded exactly like the tracker's, rounded to fp32) and
+// the points as fp32; every lane computes its cells in fp32 (FFMA + floor; differs from the
+// tracker's fp64 exact floor only within ~1e-4 voxel of a cell face), the brick offset and bounds
+// with the tracker's integer arithmetic, then issues the tracker's dependent pair: the REAL in-band
+// mask word, then the 32-byte record (record 0 when out of band).  Same item order and shape as
+// k_replay.  Counts the in-band evaluations (out[0]) so the host can check the stream.
+template <int TILES>
+__global__ __launch_bounds__(256, 2) void k_replay_gen(const float* __restrict__ poses, const float* __restrict__ pts,
+                                                       int K, int npad, int nx, int ny, int nz, unsigned sy, unsigned sz,
+                                                       const float* __restrict__ rec, const unsigned* __restrict__ mask,
+                                                       unsigned* __restrict__ queue, unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int ngroups = (npad + 32 * TILES - 1) / (32 * TILES), nch = (K + 15) / 16;
+  const int nitems = ngroups * nch;
+  float acc = 0.f;
+  unsigned ninb = 0u;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(queue, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nitems) break;
+    const int group = item / nch, chunk = item - group * nch;
+    const int k0 = chunk * 16, k1 = min(K, k0 + 16);
+    float px[TILES], py[TILES], pz[TILES];
+#pragma unroll
+    for (int p = 0; p < TILES; ++p) {
+      const int i = (group * TILES + p) * 32 + lane;
+      px[p] = py[p] = pz[p] = 0.f;
+      if (i < npad) { px[p] = __ldcg(pts + i); py[p] = __ldcg(pts + npad + i); pz[p] = __ldcg(pts + 2 * npad + i); }
+    }
+    for (int k = k0; k < k1; ++k) {
+      float m[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) m[q] = __ldg(poses + 12 * k + q);
+      uint32_t o[TILES];
+      bool ok[TILES];
+#pragma unroll
+      for (int p = 0; p < TILES; ++p) {
+        const int ix = __float2int_rd(fmaf(m[0], px[p], fmaf(m[1], py[p], fmaf(m[2], pz[p], m[3]))));
+        const int iy = __float2int_rd(fmaf(m[4], px[p], fmaf(m[5], py[p], fmaf(m[6], pz[p], m[7]))));
+        const int iz = __float2int_rd(fmaf(m[8], px[p], fmaf(m[9], py[p], fmaf(m[10], pz[p], m[11]))));
+        ok[p] = pz[p] != 0.f && (unsigned)ix <= (unsigned)(nx - 2) && (unsigned)iy <= (unsigned)(ny - 2) &&
+                (unsigned)iz <= (unsigned)(nz - 2);
+        const uint32_t off = ((uint32_t)(ix >> 2) << 6 | (uint32_t)(ix & 3)) + (uint32_t)(iy >> 2) * sy +
+                             ((uint32_t)(iy & 3) << 2) + (uint32_t)(iz >> 2) * sz + ((uint32_t)(iz & 3) << 4);
+        o[p] = off & (0u - (uint32_t)ok[p]);
+      }
+      uint32_t mw[TILES];
+#pragma unroll
+      for (int p = 0; p < TILES; ++p) mw[p] = __ldg(mask + (o[p] >> 5));
+#pragma unroll
+      for (int p = 0; p < TILES; ++p) {
+        const uint32_t inb = (mw[p] >> (o[p] & 31u)) & (uint32_t)ok[p];
+        float v[8];
+        ld32(rec + (size_t)(o[p] * inb) * 8, v);
+        acc += inb ? fabsf(v[0] + v[7]) : 0.f;
+        ninb += inb;
+      }
+    }
+  }
+  ninb = __reduce_add_sync(0xffffffffu, ninb);
+  if (lane == 0 && ninb) atomicAdd(out, (unsigned long long)ninb);
+  if (acc == 1234.5f) out[1 + blockIdx.x] = 1ull;
+}
 }  // namespace
+
+extern "C" int replay_gen_run(const float* poses, const float* pts, int K, int npad, int nx, int ny, int nz, unsigned sy,
+                              unsigned sz, const float* rec, const unsigned* mask, int reps, unsigned* queue,
+                              unsigned long long* out, float* ms_out, int tiles) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaMemset(queue, 0, 4);
+    cudaMemset(out, 0, 8);
+    cudaEventRecord(e0);
+    if (tiles == 6) k_replay_gen<6><<<296, 256>>>(poses, pts, K, npad, nx, ny, nz, sy, sz, rec, mask, queue, out);
+    else k_replay_gen<4><<<296, 256>>>(poses, pts, K, npad, nx, ny, nz, sy, sz, rec, mask, queue, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;  // the first run is a warm-up
+  }
+  *ms_out = best;
+  return (int)cudaGetLastError();
+}
 
 extern "C" int replay_run(const uint32_t* idx, int K, int npad, const float* rec, const unsigned* mask, int reps,
                           unsigned* queue, float* out, float* ms_out, int tiles) {
