@@ -214,6 +214,19 @@ __device__ __forceinline__ void member_row(double* row, double E, double Ebase, 
   }
 }
 
+// Same from a member delta (q, u) computed beforehand by member_delta: identical arithmetic.
+__device__ __forceinline__ void member_row_pre(double* row, double E, double Ebase, int rule, const double* q,
+                                               const double* u) {
+#pragma unroll
+  for (int c = 0; c < kUpdW; ++c) row[c] = 0.0;
+  if (E < Ebase) {
+    const double w = rule == 1 ? Ebase - E : 1.0;
+    row[0] = w * q[0]; row[1] = w * q[1]; row[2] = w * q[2]; row[3] = w * q[3];
+    row[4] = w * u[0]; row[5] = w * u[1]; row[6] = w * u[2];
+    row[7] = 1.0; row[8] = w;
+  }
+}
+
 // Same from the member delta precomputed in P1 (the persistent tracker's table: q(4), u(3), pad):
 // identical arithmetic, member_delta's values loaded instead of recomputed.
 __device__ __forceinline__ void member_row_tab(double* row, double E, double Ebase, int rule, const double* mrow) {
@@ -1416,6 +1429,11 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
         __syncwarp();
       }
     }
+    // the member deltas of this CTA's first P3 block depend only on s and the template rows, so
+    // they are computed here, while the other CTAs still finish P2
+    double mq[4] = {0.0, 0.0, 0.0, 0.0}, mu[3] = {0.0, 0.0, 0.0};
+    if (a.rule != 2 && tid < 256 && lb * 256 + tid < Ki)
+      member_delta(a.pst + 6 * (size_t)(lb * 256 + tid), sState[0], sState[1], mq, mu);
     if (timing) {
       __syncthreads();
       if (tid == 0) a.tdone[lb] = global_ns();
@@ -1493,6 +1511,8 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
 #ifdef PFT_MEMBER_TABLE
           member_row_tab(row, E, Ebase, a.rule, mtab + 8 * (size_t)k);
 #else
+          if (b == lb) member_row_pre(row, E, Ebase, a.rule, mq, mu);
+          else
           member_row(row, E, Ebase, a.rule, a.pst + 6 * (size_t)k, sState[0], sState[1]);
 #endif
         }
