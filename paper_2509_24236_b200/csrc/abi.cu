@@ -64,6 +64,14 @@ static cudaEvent_t ev_get() {
   return e;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PFT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void prof_begin(int cls, cudaStream_t st) {
   (void)cls;
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -266,8 +266,12 @@ __device__ __forceinline__ void prep_region(const Intr& K, double max_depth, con
 // CTAs compute the axis tables (the full sweep: tables only, nreg = 0).
 __global__ __launch_bounds__(256) void k_frame_prep(Intr K, double max_depth, const uint16_t* __restrict__ depth,
                                                     uint2* __restrict__ tiles, Pyr P, int nreg, Geom g,
-                                                    const double* __restrict__ Tdev, double4* __restrict__ tab) {
+                                                    const double* __restrict__ Tdev, double4* __restrict__ tab,
+                                                    uint32_t* __restrict__ zero, int nzero) {
   __shared__ uint2 s0[64], s1[16], s2[4];
+  pdl_wait();  // the pose (tracker output) and the previous frame's counters
+  pdl_trigger();
+  if (blockIdx.x == 0 && (int)threadIdx.x < nzero) zero[threadIdx.x] = 0u;  // the frame's counters
   if ((int)blockIdx.x >= nreg) {
     axis_entry(g, Tdev, tab, ((int)blockIdx.x - nreg) * 256 + threadIdx.x);
     return;
@@ -414,6 +418,8 @@ __device__ __forceinline__ void cull_bricks_pass(const Geom& g, const Intr& K, c
 __global__ __launch_bounds__(256) void k_cull_super(Geom g, Intr K, const double* __restrict__ Tdev,
                                                     const uint2* __restrict__ tiles, Pyr P, int nsx, int nsy, int nsz,
                                                     uint32_t* __restrict__ slist, uint32_t* __restrict__ scount) {
+  pdl_wait();
+  pdl_trigger();
   cull_super_pass(g, K, Tdev, tiles, P, nsx, nsy, nsz, slist, scount, (blockIdx.x * blockDim.x + threadIdx.x) >> 5,
                   (gridDim.x * blockDim.x) >> 5);
 }
@@ -423,6 +429,8 @@ __global__ __launch_bounds__(256) void k_cull_bricks(Geom g, Intr K, const doubl
                                                      const uint32_t* __restrict__ slist,
                                                      const uint32_t* __restrict__ scount, uint32_t* __restrict__ list,
                                                      uint32_t* __restrict__ count, uint32_t* __restrict__ nfree_out) {
+  pdl_wait();
+  pdl_trigger();
   cull_bricks_pass(g, K, Tdev, tiles, P, nsx, nsy, slist, *scount, list, count, nfree_out,
                    (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
@@ -510,6 +518,8 @@ __global__ __launch_bounds__(256, PFT_INTEG_MINB) void k_integrate_list(Geom g, 
                                                         uint32_t* __restrict__ dlist, uint32_t* __restrict__ dcount,
                                                         unsigned long long* __restrict__ nupd) {
   __shared__ unsigned sUpd;
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) sUpd = 0u;
   __syncthreads();
   fuse_pass<T>(g, K, depth, tab, list, *count, V, W, dirty, dlist, dcount, &sUpd, blockIdx.x, gridDim.x);
@@ -619,7 +629,7 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   double4* tab = (double4*)(vol->base + vol->L.axis_off);
   if (full_sweep) {
     const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
-    PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<ntab, 256, 0, st>>>(K, g.max_depth, depth, nullptr, P, 0, g, T, tab));
+    PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<ntab, 256, 0, st>>>(K, g.max_depth, depth, nullptr, P, 0, g, T, tab, nullptr, 0));
     size_t n = vol->L.elems;
     size_t blocks = (n + 255) / 256;
     int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
@@ -643,8 +653,11 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
   unsigned long long* nupd = (unsigned long long*)(vol->base + vol->L.scratch_off + 256);
   uint32_t* nfree = (uint32_t*)(vol->base + vol->L.scratch_off + 264);
   unsigned long long* bar = (unsigned long long*)(vol->base + vol->L.scratch_off + 320);
-  // kept, dirty, super-brick counts, updated voxels, free bricks, sweep flag, barrier (+64..+327)
-  cudaMemsetAsync(count, 0, 264, st);
+  // kept, dirty, super-brick counts, updated voxels, free bricks, sweep flag, barrier (+64..+327):
+  // zeroed by k_frame_prep (the fused path: here)
+  uint32_t* zero = count;
+  const int nzero = 264 / 4;
+  if (use_fused_integrate()) cudaMemsetAsync(count, 0, 264, st);
   const int nreg = P.nx(3) * P.ny(3);
   const int ntab = (4 * (g.nbx + g.nby + g.nbz) + 255) / 256;
   const int nsx = (g.nbx + kSuper - 1) / kSuper, nsy = (g.nby + kSuper - 1) / kSuper, nsz = (g.nbz + kSuper - 1) / kSuper;
@@ -670,18 +683,20 @@ pft_status integrate_impl(pft_volume* vol, const uint16_t* depth, const pft_intr
     if (e != cudaErrorCooperativeLaunchTooLarge) return fail(PFT_ERR_CUDA, "integrate launch: %s", cudaGetErrorString(e));
     cudaGetLastError();  // not sticky (SMs partly taken): the separate kernels below, same results
   }
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_frame_prep<<<nreg + ntab, 256, 0, st>>>(K, g.max_depth, depth, tiles, P, nreg, g, T, tab));
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_super<<<(ns + 255) / 256, 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, nsz, slist, scount));
-  PFT_LAUNCH(PFT_PROF_CULL, st, k_cull_bricks<<<resident_grid(k_cull_bricks, 256), 256, 0, st>>>(g, K, T, tiles, P, nsx, nsy, slist, scount, list, count, nfree));
+  PFT_LAUNCH(PFT_PROF_CULL, st, launch_pdl(k_frame_prep, dim3(nreg + ntab), dim3(256), 0, st, K, g.max_depth, depth, tiles, P, nreg, g, T, tab, zero, nzero));
+  PFT_LAUNCH(PFT_PROF_CULL, st, launch_pdl(k_cull_super, dim3((ns + 255) / 256), dim3(256), 0, st, g, K, T, (const uint2*)tiles, P, nsx, nsy, nsz, slist, scount));
+  PFT_LAUNCH(PFT_PROF_CULL, st, launch_pdl(k_cull_bricks, dim3(resident_grid(k_cull_bricks, 256)), dim3(256), 0, st, g, K, T, (const uint2*)tiles, P, nsx, nsy, (const uint32_t*)slist, (const uint32_t*)scount, list, count, nfree));
   // grid = the resident capacity (one wave: no partial second wave of CTAs, the CTA-stride loop
   // balances the bricks)
   const int grid = vol->esize == 4 ? resident_grid(k_integrate_list<float>, 256) : resident_grid(k_integrate_list<__half>, 256);
   if (vol->esize == 4)
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<float><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (float*)(vol->base + vol->L.v_off),
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, launch_pdl(k_integrate_list<float>, dim3(grid), dim3(256), 0, st, g, K, depth, (const double4*)tab,
+                                                  (const uint32_t*)list, (const uint32_t*)count, (float*)(vol->base + vol->L.v_off),
                                                   (float*)(vol->base + vol->L.w_off), dirty, dlist, dcount, nupd));
   else
-    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, k_integrate_list<__half><<<grid, 256, 0, st>>>(g, K, depth, tab, list, count, (__half*)(vol->base + vol->L.v_off),
-                                                   (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount, nupd));
+    PFT_LAUNCH(PFT_PROF_INTEGRATE, st, launch_pdl(k_integrate_list<__half>, dim3(grid), dim3(256), 0, st, g, K, depth, (const double4*)tab,
+                                                  (const uint32_t*)list, (const uint32_t*)count, (__half*)(vol->base + vol->L.v_off),
+                                                  (__half*)(vol->base + vol->L.w_off), dirty, dlist, dcount, nupd));
   records_rebuild_dirty(vol, st);
   return cuda_check("integrate");
 }

@@ -56,6 +56,31 @@ struct VolLayout {
 
 namespace pft {
 constexpr int kMaxFusedRanks = PFT_MAX_FUSED_RANKS;  // F2 fused exchange: ranks per job
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// The integration chain (frame prep -> culls -> fusion -> record refresh) launches each kernel with
+// programmatic stream serialization: its CTAs are scheduled while the previous kernel drains and
+// wait in pdl_wait() (griddepcontrol.wait: the previous grid has completed and its memory is
+// visible) before touching anything it wrote; pdl_trigger() lets the next kernel be launched
+// early.  Without the launch attribute both are no-ops.  Every grid of the chain fits in one wave,
+// so early-launched CTAs never hold SM slots a predecessor still needs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // PFT_PDL=0 disables (abi.cu)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 }
 
 struct pft_volume {

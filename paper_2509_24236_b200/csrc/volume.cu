@@ -114,6 +114,8 @@ __global__ __launch_bounds__(256) void k_records_dirty(Geom g, const T* __restri
                                                        uint32_t* __restrict__ mask, uint32_t* __restrict__ dirty,
                                                        const uint32_t* __restrict__ dlist,
                                                        const uint32_t* __restrict__ dcount) {
+  pdl_wait();  // the fusion kernel's dirty list
+  pdl_trigger();
   records_dirty_pass<T>(g, V, R, mask, dirty, dlist, *dcount, blockIdx.x, gridDim.x);
 }
 
@@ -207,9 +209,9 @@ void records_rebuild_dirty(pft_volume* vol, cudaStream_t st) {
   const uint32_t* dlist = (const uint32_t*)(vol->base + vol->L.dlist_off);
   const uint32_t* dcount = (const uint32_t*)(vol->base + vol->L.scratch_off + 128);
   if (vol->esize == 4)
-    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_dirty<float><<<grid, 256, 0, st>>>(vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, launch_pdl(k_records_dirty<float>, dim3(grid), dim3(256), 0, st, vol->g, (const float*)(vol->base + vol->L.v_off), (float*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
   else
-    PFT_LAUNCH(PFT_PROF_RECORDS, st, k_records_dirty<__half><<<grid, 256, 0, st>>>(vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
+    PFT_LAUNCH(PFT_PROF_RECORDS, st, launch_pdl(k_records_dirty<__half>, dim3(grid), dim3(256), 0, st, vol->g, (const __half*)(vol->base + vol->L.v_off), (__half*)(vol->base + vol->L.r_off), (uint32_t*)(vol->base + vol->L.m_off), dirty, dlist, dcount));
 }
 
 }  // namespace pft
