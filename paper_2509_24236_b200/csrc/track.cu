@@ -1550,7 +1550,19 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       if (tid == 8) red[8][0] = __ldcg(tkout + 7);  // weight sum = number selected
       __syncthreads();
     } else {
-      if (tid < 256) {
+      if (nblk <= 256) {
+        // every CTA reads the same nblk x kUpdW partials right after the barrier: read them as one
+        // flat array, consecutive threads on consecutive doubles (a few 128-B requests per CTA
+        // instead of ~45 scattered ones on the same 5 L2 lines, x 296 CTAs); red[c][b] = 0 + p
+        if (tid < 256)
+#pragma unroll
+          for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
+        __syncthreads();
+        for (int e = tid; e < nblk * kUpdW; e += kPT) {
+          const int b = e / kUpdW, c = e - b * kUpdW;
+          red[c][b] += __ldcg(upart + e);
+        }
+      } else if (tid < 256) {
 #pragma unroll
         for (int c = 0; c < kUpdW; ++c) red[c][tid] = 0.0;
         for (int b = tid; b < nblk; b += 256)
