@@ -1191,6 +1191,10 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
   int* const pflag = (int*)(wsb + a.o_pflag);
   double* const upart = (double*)(wsb + a.o_upart);
   unsigned long long* const cpart = (unsigned long long*)(wsb + a.o_cpart);
+  // centre-sum ring slot q: S at CSLOT(q)[0], n at CSLOT(q)[CN] (S and n on separate 128-B lines
+  // measured the same)
+#define CN 1
+#define CSLOT(q) (cpart + 2 * (q))
   unsigned* const work = (unsigned*)(wsb + a.o_work);
   unsigned long long* const ckey = (unsigned long long*)(wsb + a.o_ckey);
   int* const cidx = (int*)(wsb + a.o_cidx);
@@ -1254,7 +1258,7 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     for (int sft = 16; sft > 0; sft >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, sft));
     if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
     for (int k = lb * kPT + tid; k < kloc; k += stride) { acc[k].S = 0ull; acc[k].n = 0u; }
-    if (lb == 0 && tid == 0) { cpart[0] = 0ull; cpart[1] = 0ull; }
+    if (lb == 0 && tid == 0) { CSLOT(0)[0] = 0ull; CSLOT(0)[CN] = 0ull; }
   }
   if (tid == 0) {
     for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
@@ -1270,13 +1274,16 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
   }
   PFT_TMARK(7);
   const double pmax = __longlong_as_double((long long)__ldcg(&st->pmax_bits));
+  __shared__ int sNv[4];  // valid points per set (final after P0's barrier): one read per CTA, not
+  if (tid < 4) sNv[tid] = __ldcg(&st->Nvalid[tid]);  // one per warp of every CTA and iteration
+  __syncthreads();
   int it = 0;
   for (; it < a.iters; ++it) {
     const int j = it % nsched;
     const int Ki = sSchedK[j], set = sSchedSet[j];
     const PSet ps = sSets[set];
     const Points pts = ps.pts();
-    const int N = __ldcg(&st->Nvalid[set]);
+    const int N = sNv[set];
     // ---- B: baseline E(P^(i-1)) on this iteration's point set when it changed (L11)
     if (set != sSet) {
       if (tid == 0) sFlagC = explicit_pose(sP, a.g, pmax, sM);
@@ -1287,16 +1294,16 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       unsigned long long S;
       unsigned n;
       block_total<kPT>(sum, cnt, sS, sNw, S, n);
-      unsigned long long* slot = cpart + 2 * (cev % 3);
+      unsigned long long* slot = CSLOT(cev % 3);
       if (tid == 0) {
-        if (lb == 0) { cpart[2 * ((cev + 1) % 3)] = 0ull; cpart[2 * ((cev + 1) % 3) + 1] = 0ull; }
+        if (lb == 0) { CSLOT((cev + 1) % 3)[0] = 0ull; CSLOT((cev + 1) % 3)[CN] = 0ull; }
         atomicAdd(slot, S);
-        atomicAdd(slot + 1, (unsigned long long)n);
+        atomicAdd(slot + CN, (unsigned long long)n);
       }
       grid_barrier(st, gen, nb, a.watchdog_ns);
       ++cev;
       unsigned long long S2 = 0ull, n2 = 0ull;
-      if (tid == 0) { S2 = __ldcg(slot); n2 = __ldcg(slot + 1); }
+      if (tid == 0) { S2 = __ldcg(slot); n2 = __ldcg(slot + CN); }
       if (tid == 0) {
         sState[2] = fitness_c(S2, (unsigned)n2, a.rho, N);
         sNc = (unsigned)n2;
@@ -1595,9 +1602,9 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       unsigned n;
       block_total<kPT>(sum, cnt, sS, sNw, S, n);
       if (tid == 0) {
-        if (lb == 0) { cpart[2 * ((cev + 1) % 3)] = 0ull; cpart[2 * ((cev + 1) % 3) + 1] = 0ull; }
-        atomicAdd(cpart + 2 * (cev % 3), S);
-        atomicAdd(cpart + 2 * (cev % 3) + 1, (unsigned long long)n);
+        if (lb == 0) { CSLOT((cev + 1) % 3)[0] = 0ull; CSLOT((cev + 1) % 3)[CN] = 0ull; }
+        atomicAdd(CSLOT(cev % 3), S);
+        atomicAdd(CSLOT(cev % 3) + CN, (unsigned long long)n);
       }
       grid_barrier(st, gen, nb, a.watchdog_ns);  // sNA is identical in every CTA: uniform barrier
     }
@@ -1605,7 +1612,7 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     // ---- P5: E(P), F3 guard, s-law, stalls, stop rule, trace
     unsigned long long S5 = 0ull, n5 = 0ull;
     if (sNA > 0) {
-      if (tid == 0) { S5 = __ldcg(cpart + 2 * (cev % 3)); n5 = __ldcg(cpart + 2 * (cev % 3) + 1); }
+      if (tid == 0) { S5 = __ldcg(CSLOT(cev % 3)); n5 = __ldcg(CSLOT(cev % 3) + CN); }
       ++cev;
     }
     if (tid == 0) {
@@ -1646,6 +1653,8 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
            it, (int)nb, tph[7] * 1e-3, tph[0] * 1e-3, tph[1] * 1e-3, tph[2] * 1e-3, tph[6] * 1e-3,
            tph[3] * 1e-3, tph[4] * 1e-3, tph[5] * 1e-3);
 #undef PFT_TMARK
+#undef CSLOT
+#undef CN
   // ---- outputs
   if (lb == 0 && tid == 0) {
     for (int q = 0; q < 12; ++q) st->P[q] = sP[q];
