@@ -802,6 +802,24 @@ def test_integrate_fused_launch_identical(storage, tmp_path):
     assert outs["0"]["stats"][:, 2].min() > 1000
 
 
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_integrate_pdl_launch_identical(storage, tmp_path):
+    """The integration chain launched with programmatic dependent launch (default) and as plain
+    stream-ordered kernels (PFT_PDL=0): bit-identical volumes, checksums and work counters (each
+    kernel waits on griddepcontrol before reading its predecessor's output)."""
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_integrate.py")
+    outs = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"{storage}_pdl{mode}.npz")
+        subprocess.check_call([sys.executable, helper, storage, f], env=dict(os.environ, PFT_PDL=mode))
+        outs[mode] = np.load(f)
+    for k in ("V", "W", "stats", "checksum"):
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
+    assert outs["0"]["stats"][:, 2].min() > 1000
+
+
 @pytest.mark.parametrize("case", ["ragged", "far_principal_point", "tiny_image", "huge_image"])
 def test_integrate_edge_cases(pft, case):
     """Culled integration edge cases against the full sweep and the oracle, bit for bit:
