@@ -1236,6 +1236,11 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
   __syncthreads();
   const int nsched = a.sc.n, nsets = a.sc.nsets;
   const unsigned long long xround0 = sXround;
+#ifndef PFT_CENTRE_CTAS
+#define PFT_CENTRE_CTAS 148  // one slice per SM: 1.4233 vs 1.4249 ms (all 296 CTAs) and 1.4241 (96), A/B
+#endif
+  // CTAs that evaluate the centre E(P) (slices of the point set); the others add nothing
+  const int ncc = PFT_CENTRE_CTAS > 0 ? min(nb, PFT_CENTRE_CTAS) : nb;
   // ---- P0: points of every set (a1/a2), accumulators, pmax
   {
     const int stride = nb * kPT;
@@ -1290,15 +1295,17 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       __syncthreads();
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt);
+      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, ncc, lb, sum, cnt);
       unsigned long long S;
       unsigned n;
       block_total<kPT>(sum, cnt, sS, sNw, S, n);
       unsigned long long* slot = CSLOT(cev % 3);
       if (tid == 0) {
         if (lb == 0) { CSLOT((cev + 1) % 3)[0] = 0ull; CSLOT((cev + 1) % 3)[CN] = 0ull; }
-        atomicAdd(slot, S);
-        atomicAdd(slot + CN, (unsigned long long)n);
+        if (lb < ncc) {
+          atomicAdd(slot, S);
+          atomicAdd(slot + CN, (unsigned long long)n);
+        }
       }
       grid_barrier(st, gen, nb, a.watchdog_ns);
       ++cev;
@@ -1542,7 +1549,7 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     // the centre slice's first-pass points, loaded now: their L2 round trip overlaps the barrier
     double cpre[3] = {0.0, 0.0, 0.0};
     {
-      const int per = (pts.npad + nb - 1) / nb, i = lb * per + tid;
+      const int per = (pts.npad + ncc - 1) / ncc, i = lb * per + tid;
       if (i < min(pts.npad, lb * per + per)) { cpre[0] = __ldcg(pts.x + i); cpre[1] = __ldcg(pts.y + i); cpre[2] = __ldcg(pts.z + i); }
     }
     grid_barrier(st, gen, nb, a.watchdog_ns);
@@ -1597,14 +1604,16 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     if (sNA > 0) {
       unsigned long long sum = 0ull;
       unsigned cnt = 0u;
-      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, nb, lb, sum, cnt, cpre);
+      centre_slice<T, kPT>((const T*)a.V, a.mask, a.g, pts, sM, sFlagC, ncc, lb, sum, cnt, cpre);
       unsigned long long S;
       unsigned n;
       block_total<kPT>(sum, cnt, sS, sNw, S, n);
       if (tid == 0) {
         if (lb == 0) { CSLOT((cev + 1) % 3)[0] = 0ull; CSLOT((cev + 1) % 3)[CN] = 0ull; }
-        atomicAdd(CSLOT(cev % 3), S);
-        atomicAdd(CSLOT(cev % 3) + CN, (unsigned long long)n);
+        if (lb < ncc) {
+          atomicAdd(CSLOT(cev % 3), S);
+          atomicAdd(CSLOT(cev % 3) + CN, (unsigned long long)n);
+        }
       }
       grid_barrier(st, gen, nb, a.watchdog_ns);  // sNA is identical in every CTA: uniform barrier
     }
