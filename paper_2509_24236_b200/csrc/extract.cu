@@ -44,7 +44,7 @@ template <> __device__ __forceinline__ void ld_w2<__half>(const __half* p, float
 // 0.25 ms on the bench map (0.21 -> 0.35 of HBM for W of every voxel + V of the observed ones);
 // the rest is the observed bricks' round trips, one brick at a time per warp.
 #ifndef PFT_EXTRACT_MINB
-#define PFT_EXTRACT_MINB 6  // 40 registers, 48 warps/SM: 0.250 ms vs 0.289 (8: 32 registers, spills) and 0.383 (4) on the bench map
+#define PFT_EXTRACT_MINB 6  // 40 registers, 48 warps/SM: 0.250 ms vs 0.301 at 8 CTAs/SM (32 registers) on the bench map
 #endif
 template <typename T>
 __global__ __launch_bounds__(256, PFT_EXTRACT_MINB) void k_extract(Geom g, const T* __restrict__ V, const T* __restrict__ W,
