@@ -20,6 +20,11 @@ def make_case(cfg, seed):
         c["params"] = dataclasses.replace(c["params"], iters=7, nsched=3, sched_K=(64, 40, 24, 0),
                                           sched_sx=(1, 2, 4, 0), sched_sy=(1, 2, 2, 0), guard=1, update_rule=1,
                                           stall_limit=3, min_search_deg=0.05, min_search_cm=0.05)
+    if cfg == "tiny_bigK":
+        # more than 256 update blocks of 256 particles: the combine's general path (K > 65536)
+        from synth.configs import make_pst
+        c["pst"] = make_pst(seed, 70000)
+        c["params"] = dataclasses.replace(c["params"], iters=2)
     if cfg == "tiny16":
         c = with_desc(c, storage="f16")
         c["V"], c["W"] = c["V"].astype(np.float16), c["W"].astype(np.float16)

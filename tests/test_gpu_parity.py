@@ -459,7 +459,7 @@ def test_sequence_track_then_integrate(pft):
     vol.close()
 
 
-@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single", "tiny_sched", "single_topk"])
+@pytest.mark.parametrize("cfg", ["tiny", "tiny16", "single", "tiny_sched", "single_topk", "tiny_bigK"])
 def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
     """The single-launch persistent tracker (G = 1 default) and the multi-launch path (used for
     G > 1) share their arithmetic helpers and fixed reduction trees: outputs must be bit-identical."""
