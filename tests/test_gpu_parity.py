@@ -592,6 +592,28 @@ def test_extract_surface_bit_exact(pft, storage):
     vt.close()
 
 
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_extract_surface_dense_crossings(pft, storage):
+    """A checkerboard volume (every voxel pair with a sign change, ragged 18 x 13 x 11 grid): up to 3
+    crossings per voxel, more than a warp's 64-point shared-memory buffer holds for one brick (the
+    kernel's direct-append path) and several buffer flushes per warp; bit-equal to the oracle."""
+    nx, ny, nz = 18, 13, 11
+    desc = VolumeDesc(nx, ny, nz, 0.05, (-0.4, -0.3, -0.2), 0.15, storage=storage)
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    V = np.where((i + j + k) % 2 == 0, 0.5, -0.25).astype(np.float32)
+    V[2, 3, 4] = 0.0  # a zero value: crossings with it count only against a non-zero neighbour
+    W = np.ones_like(V)
+    W[5, 6, 7] = 0.0  # an unobserved voxel breaks its crossings
+    if storage == "f16":
+        V, W = V.astype(np.float16), W.astype(np.float16)
+    vol = gpu_volume(pft, desc, V, W)
+    g = vol.extract_surface().cpu().numpy()
+    o = oracle.OracleVolume(desc, V, W).extract()
+    assert len(o) > 3 * nx * ny * nz // 2 and len(g) == len(o)
+    assert np.array_equal(_sorted_rows(g), _sorted_rows(o))
+    vol.close()
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_virtual_shards_bit_identical(pft, G):  # noqa: C901
     """SURVEY.md §4 "virtual shards": the multi-GPU code path (rank q evaluates template rows
