@@ -283,6 +283,8 @@ def run_ours(args):
     host_depth = {t: torch.from_numpy(frames[t]["depth"]).pin_memory() for t in idx}
     host_rel = {t: torch.from_numpy(frames[t]["rel"].copy()).pin_memory() for t in idx}
     host_T = [torch.empty(3, 4, dtype=torch.float64).pin_memory() for _ in idx]
+    eye = torch.zeros(3, 4, dtype=torch.float64, device=dev)
+    eye[0, 0] = eye[1, 1] = eye[2, 2] = 1.0
     d_buf = gd if graphs else [torch.empty_like(dev_in[idx[0]][0]) for _ in range(2)]
     r_buf = gr if graphs else [torch.empty_like(dev_in[idx[0]][1]) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
@@ -318,7 +320,11 @@ def run_ours(args):
         else:
             step(d_buf[b], r_buf[b])
         used[b].record(stream)
-        host_T[j].copy_(out["T"], non_blocking=True)
+        # the tracked pose to pinned host memory: written by a library kernel through the pinned
+        # buffer's unified-address mapping (pft_pose_compose with an identity right factor, an exact
+        # copy) -- 96 B over PCIe per step; ~9 us less than a memcpy node (3 bench runs each:
+        # e2e 1.505 vs 1.514 ms per step; tools/e2e_split.py)
+        pft.pose_compose(out["T"], eye, out=host_T[j])
         ev2[j][1].record(stream)
     barrier()
     poses["e2e"] = np.stack([h.numpy() for h in host_T])
