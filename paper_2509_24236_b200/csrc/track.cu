@@ -1077,6 +1077,11 @@ struct PArgsX {
   size_t pre_off;
 };
 
+#ifdef PFT_WARP_UTIL
+// diagnostic build only: per-warp P2 time split (claim -> staged, evaluation loop, row reduction,
+// idle after the queue ran dry until the P2 barrier released), ns summed over the launch
+__device__ unsigned long long g_wutil[4096][4];
+#endif
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1091,9 +1096,24 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 // Grid barrier over the nb co-resident CTAs of one rank: a monotone arrival counter (zeroed with
 // the state before every launch).  Thread 0 adds 1 with release semantics (MEMBAR.GPU + RED)
-// and polls with acquire loads (LDG.STRONG.GPU + CCTL.IVALL, so data other CTAs wrote before the
-// barrier is read fresh after it) until all nb CTAs of this round arrived: 1.3 us vs 2.2 us for
-// a sense-reversing barrier at 296 CTAs (tools/microbench/barrier.cu).
+// and polls until all nb CTAs of this round arrived: 1.3 us vs 2.2 us for a sense-reversing
+// barrier at 296 CTAs (tools/microbench/barrier.cu).  The poll is a relaxed load (LDG.STRONG.GPU)
+// and ONE acquire load follows it (LDG.STRONG.GPU + CCTL.IVALL, so data other CTAs wrote before
+// the barrier is read fresh after it): an acquire in the poll loop itself invalidated the SM's L1
+// on every poll, under the records the co-resident CTA was still gathering in P2
+// (PFT_POLL_ACQUIRE=1 restores it, for A/B).
+#ifndef PFT_POLL_ACQUIRE
+#define PFT_POLL_ACQUIRE 0
+#endif
+__device__ __forceinline__ unsigned long long ld_poll_gpu(const unsigned long long* p) {
+  unsigned long long v;
+#if PFT_POLL_ACQUIRE
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#else
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#endif
+  return v;
+}
 // Watchdog: a CTA that waits longer than watchdog_ns (PFT_WATCHDOG_MS, default 5 s) traps (a launch
 // error instead of a hung GPU).
 __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long& target, int nb,
@@ -1104,7 +1124,7 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&st->bar_mono) : "memory");
     unsigned long long v, t0 = 0ull;
     for (;;) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&st->bar_mono) : "memory");
+      v = ld_poll_gpu(&st->bar_mono);
       if (v >= target) break;
       __nanosleep(32);
       const unsigned long long now = global_ns();
@@ -1114,6 +1134,11 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
         __trap();
       }
     }
+#if !PFT_POLL_ACQUIRE
+    // the acquire half: reads a value >= target of the same monotone counter, i.e. the release
+    // sequence of every arrival of this round
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&st->bar_mono) : "memory");
+#endif
   }
   __syncthreads();
 }
@@ -1367,7 +1392,13 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       const int r1 = (int)((long long)nitems * (lb + 1) / nb);
       if (tid == 0) sItem = 0;
       __syncthreads();
+#ifdef PFT_WARP_UTIL
+      unsigned long long wu0 = global_ns(), wu[4] = {0ull, 0ull, 0ull, 0ull};
+#endif
       for (;;) {
+#ifdef PFT_WARP_UTIL
+        const unsigned long long wa = global_ns();
+#endif
         int item = 0;
         if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(work + it, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
@@ -1400,6 +1431,9 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
         const int myflag = lane < k1 - k0 ? __ldcg(pflag + kb + k0 + lane) : 0;
         const unsigned fvalid = __ballot_sync(0xffffffffu, myflag != 0), ffast = __ballot_sync(0xffffffffu, myflag == 2);
         __syncwarp();
+#ifdef PFT_WARP_UTIL
+        const unsigned long long wb = global_ns();
+#endif
         unsigned long long (*part)[33] = sPart[tid >> 5];
         for (int k = k0; k < k1; ++k) {
           unsigned sum = 0u;
@@ -1418,6 +1452,9 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
           part[k - k0][lane] = (unsigned long long)sum | ((unsigned long long)cnt << 32);
         }
         __syncwarp();
+#ifdef PFT_WARP_UTIL
+        const unsigned long long wc = global_ns();
+#endif
         // particle j's row is reduced by lanes j and j + 16, half a row each (exact integers),
         // combined by one shuffle; lane j issues the atomics
         static_assert(kItemParticles <= 16, "two lanes per particle row");
@@ -1441,7 +1478,18 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
           }
         }
         __syncwarp();
+#ifdef PFT_WARP_UTIL
+        wu[0] += wb - wa; wu[1] += wc - wb; wu[2] += global_ns() - wc;
+#endif
       }
+#ifdef PFT_WARP_UTIL
+      wu0 = global_ns();
+      if (lane == 0) {
+        const int gw = (lb * kPT + tid) >> 5;
+        g_wutil[gw][0] += wu[0]; g_wutil[gw][1] += wu[1]; g_wutil[gw][2] += wu[2];
+        g_wutil[gw][3] -= wu0;  // + the P2 barrier release time below
+      }
+#endif
     }
     // the member deltas of this CTA's first P3 block depend only on s and the template rows, so
     // they are computed here, while the other CTAs still finish P2
@@ -1453,6 +1501,9 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       if (tid == 0) a.tdone[lb] = global_ns();
     }
     grid_barrier(st, gen, nb, a.watchdog_ns);
+#ifdef PFT_WARP_UTIL
+    if ((tid & 31) == 0) g_wutil[(lb * kPT + tid) >> 5][3] += global_ns();
+#endif
     if (timing && tid == 0 && lb == 0) {
       unsigned long long lo = ~0ull, hi = 0ull;
       for (int b = 0; b < (int)nb; ++b) {
@@ -1996,6 +2047,22 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
     return PFT_ERR_UNSUPPORTED;  // the caller falls back to the multi-launch tracker
   }
   if (e != cudaSuccess) return fail(PFT_ERR_CUDA, "persistent tracker launch: %s", cudaGetErrorString(e));
+#ifdef PFT_WARP_UTIL
+  {
+    static unsigned long long h[4096][4];
+    cudaStreamSynchronize(c.st);
+    cudaMemcpyFromSymbol(h, g_wutil, sizeof h);
+    const int nw = grid * (kPT / 32);
+    double t[4] = {0, 0, 0, 0};
+    for (int w = 0; w < nw; ++w)
+      for (int q = 0; q < 4; ++q) t[q] += (double)h[w][q];
+    const double tot = t[0] + t[1] + t[2] + t[3];
+    printf("pft warp util (P2, per warp, us per launch): staging %.1f  eval %.1f  reduce %.1f  idle-at-end %.1f  (eval share %.3f)\n",
+           t[0] / nw * 1e-3, t[1] / nw * 1e-3, t[2] / nw * 1e-3, t[3] / nw * 1e-3, t[1] / tot);
+    static unsigned long long zero[4096][4];
+    cudaMemcpyToSymbol(g_wutil, zero, sizeof zero);
+  }
+#endif
   return cuda_check("track (persistent)");
 }
 
