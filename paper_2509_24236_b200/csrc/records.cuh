@@ -58,8 +58,12 @@ __device__ __forceinline__ void records_dirty_pass(const Geom& g, const T* __res
                                                    const uint32_t* __restrict__ dlist, uint32_t n, uint32_t block,
                                                    uint32_t nblocks) {
   const uint32_t w = threadIdx.x & 63;
-  for (uint32_t li = block * 4 + (threadIdx.x >> 6); li < n; li += nblocks * 4) {
-    const uint32_t b = dlist[li];
+  const uint32_t step = nblocks * 4;
+  uint32_t li = block * 4 + (threadIdx.x >> 6);
+  uint32_t bn = li < n ? __ldcg(dlist + li) : 0u;
+  for (; li < n; li += step) {
+    const uint32_t b = bn;
+    if (li + step < n) bn = __ldcg(dlist + li + step);  // the next cell-brick, in flight during this one
 #ifdef PFT_DEBUG
     if (b >= (uint32_t)g.nbx * g.nby * g.nbz) {
       printf("pft debug: bad dirty cell-brick %u\n", b);
