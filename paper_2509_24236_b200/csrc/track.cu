@@ -1105,6 +1105,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
 #ifndef PFT_POLL_ACQUIRE
 #define PFT_POLL_ACQUIRE 0
 #endif
+#ifndef PFT_POLL_NS
+#define PFT_POLL_NS 32  // poll backoff
+#endif
 __device__ __forceinline__ unsigned long long ld_poll_gpu(const unsigned long long* p) {
   unsigned long long v;
 #if PFT_POLL_ACQUIRE
@@ -1126,7 +1129,7 @@ __device__ __forceinline__ void grid_barrier(TrackState* st, unsigned long long&
     for (;;) {
       v = ld_poll_gpu(&st->bar_mono);
       if (v >= target) break;
-      __nanosleep(32);
+      if (PFT_POLL_NS > 0) __nanosleep(PFT_POLL_NS);
       const unsigned long long now = global_ns();
       if (t0 == 0ull) t0 = now;
       else if (now - t0 > watchdog_ns) {
