@@ -1398,12 +1398,17 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
 #ifdef PFT_WARP_UTIL
       unsigned long long wu0 = global_ns(), wu[4] = {0ull, 0ull, 0ull, 0ull};
 #endif
+      // sched 0: a warp's first item of the phase is its own index (no atomic: the 2368 first
+      // claims no longer queue on one L2 address at the phase start); later ones come from the queue
+      const int nwq = nb * (kPT / 32), gwq = lb * (kPT / 32) + (tid >> 5);
+      bool first = true;
       for (;;) {
 #ifdef PFT_WARP_UTIL
         const unsigned long long wa = global_ns();
 #endif
         int item = 0;
-        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : (int)atomicAdd(work + it, 1u);
+        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : first ? gwq : nwq + (int)atomicAdd(work + it, 1u);
+        first = false;
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (a.sched == 1 ? r1 : nitems)) break;
         int group, k0, k1;
