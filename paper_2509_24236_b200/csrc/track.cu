@@ -1398,17 +1398,30 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
 #ifdef PFT_WARP_UTIL
       unsigned long long wu0 = global_ns(), wu[4] = {0ull, 0ull, 0ull, 0ull};
 #endif
-      // sched 0: a warp's first item of the phase is its own index (no atomic: the 2368 first
-      // claims no longer queue on one L2 address at the phase start); later ones come from the queue
+      // sched 0: the first ~static_pct % of the big items are handed out statically, warp w taking
+      // items w, w + nw, w + 2 nw, ... (no atomic round trip per claim, and the 8 warps of a CTA --
+      // consecutive items -- work on the same point group, sharing its points and nearby records
+      // in L1); the rest, and the small tail items, come from the dynamic queue, whose counter is
+      // offset by the static items
       const int nwq = nb * (kPT / 32), gwq = lb * (kPT / 32) + (tid >> 5);
-      bool first = true;
+#ifndef PFT_STATIC_ITEMS
+#define PFT_STATIC_ITEMS 4  // at most, per warp (config Q: 4 of ~6.3 items; 2 / 3 / 5: slower, A/B)
+#endif
+#ifndef PFT_STATIC_PCT
+#define PFT_STATIC_PCT 80   // at most this share of the big items (5 at config Q = 98%: slower)
+#endif
+      const int nstat = a.sched == 1 ? 0 : min(PFT_STATIC_ITEMS, (int)((long long)nbig * PFT_STATIC_PCT / 100) / nwq);
+      int nst = 0;
       for (;;) {
 #ifdef PFT_WARP_UTIL
         const unsigned long long wa = global_ns();
 #endif
         int item = 0;
-        if (lane == 0) item = a.sched == 1 ? r0 + atomicAdd(&sItem, 1) : first ? gwq : nwq + (int)atomicAdd(work + it, 1u);
-        first = false;
+        if (lane == 0)
+          item = a.sched == 1                ? r0 + atomicAdd(&sItem, 1)
+                 : nst < nstat ? gwq + nst * nwq
+                                : nstat * nwq + (int)atomicAdd(work + it, 1u);
+        ++nst;
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= (a.sched == 1 ? r1 : nitems)) break;
         int group, k0, k1;
