@@ -149,6 +149,9 @@ struct TrackState {
   unsigned int ticket_upd, ticket_ctr;
   unsigned long long pmax_bits;  // max |point coordinate| over all sets (persistent path)
   unsigned long long bar_mono;      // persistent path: grid-barrier arrivals (monotone within a launch)
+  unsigned int sm_cnt[256];   // persistent path, SM pairing: CTAs arrived per SM id
+  unsigned int sm_pair[256];  //   pair index + 1 of the SM (published by its first CTA)
+  unsigned int npairs, pad2;
   double pad[4];
 };
 

@@ -1045,7 +1045,7 @@ struct PArgs {
   BPFrame f;
   Sched sc;
   const float* pst;
-  int K, conv, iters, rule, guard, sched, tail_pct;
+  int K, conv, iters, rule, guard, sched, tail_pct, pair_sm;
   double beta, rho, omega0, v0;
   StopRule sr;
   const double* T_init;
@@ -1191,7 +1191,7 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
   double (*red)[256] = reinterpret_cast<double (*)[256]>(sUnion);
   __shared__ double sP[12], sM[12], sPprev[12];
   __shared__ double sState[4];  // omega, v, Ec, Ebase
-  __shared__ int sFlagC, sNA, sItem, sStalls, sStop, sSet, sKlast, sRej;
+  __shared__ int sFlagC, sNA, sItem, sPos, sStalls, sStop, sSet, sKlast, sRej;
   __shared__ unsigned sNc, sNcBase;
   __shared__ unsigned long long sS[kPT / 32];
   __shared__ unsigned sNw[kPT / 32];
@@ -1292,6 +1292,33 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     if (lane == 0 && pm > 0.0) atomicMax(&st->pmax_bits, (unsigned long long)__double_as_longlong(pm));
     for (int k = lb * kPT + tid; k < kloc; k += stride) { acc[k].S = 0ull; acc[k].n = 0u; }
     if (lb == 0 && tid == 0) { CSLOT(0)[0] = 0ull; CSLOT(0)[CN] = 0ull; }
+    // P2's static items go to CTA positions; with exactly two co-resident CTAs on every SM
+    // (a.pair_sm: grid = 2 x SMs, so each SM holds two) the two CTAs of an SM take adjacent
+    // positions, so its 16 warps share one point group in their L1.  Pairing: the SM's first CTA
+    // draws a pair index and publishes it, the second waits for it.
+    if (tid == 0) {
+      int pos = lb;
+      unsigned smid, nsm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+      if (a.pair_sm && nsm <= 256u) {
+        const unsigned sl = atomicAdd(&st->sm_cnt[smid], 1u);
+        unsigned pr;
+        if (sl == 0u) {
+          pr = atomicAdd(&st->npairs, 1u);
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&st->sm_pair[smid]), "r"(pr + 1u) : "memory");
+        } else {
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(pr) : "l"(&st->sm_pair[smid]) : "memory");
+            if (pr) break;
+            __nanosleep(32);
+          }
+          pr -= 1u;
+        }
+        pos = (int)(pr * 2u + (sl & 1u));
+      }
+      sPos = pos;
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < 12; ++q) sP[q] = a.T_init[q];
@@ -1403,7 +1430,7 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
       // consecutive items -- work on the same point group, sharing its points and nearby records
       // in L1); the rest, and the small tail items, come from the dynamic queue, whose counter is
       // offset by the static items
-      const int nwq = nb * (kPT / 32), gwq = lb * (kPT / 32) + (tid >> 5);
+      const int nwq = nb * (kPT / 32), gwq = sPos * (kPT / 32) + (tid >> 5);
 #ifndef PFT_STATIC_ITEMS
 #define PFT_STATIC_ITEMS 4  // at most, per warp (config Q: 4 of ~6.3 items; 2 / 3 / 5: slower, A/B)
 #endif
@@ -2009,6 +2036,13 @@ static pft_status track_persistent(Launch& c, const uint16_t* depth, const pft_i
   pa.sched = sched;
   static const int tail_pct = [] { const char* e = getenv("PFT_TAIL_PCT"); return e ? atoi(e) : 5; }();
   pa.tail_pct = tail_pct;
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const bool pair_env = [] { const char* e = getenv("PFT_PAIR_SM"); return !(e && e[0] == '0'); }();
+    pa.pair_sm = (pair_env && !emul && G == 1 && grid == 2 * sms) ? 1 : 0;
+  }
   pa.beta = prm->beta; pa.rho = prm->min_inband_frac; pa.omega0 = prm->omega0_deg; pa.v0 = prm->v0_cm;
   pa.sr = StopRule{prm->min_search_deg, prm->min_search_cm, prm->stall_limit};
   pa.T_init = T_init;
