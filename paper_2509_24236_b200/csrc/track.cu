@@ -1295,7 +1295,9 @@ __global__ __launch_bounds__(kPT, PFT_PERSIST_MINB) void k_track_persistent(PArg
     // P2's static items go to CTA positions; with exactly two co-resident CTAs on every SM
     // (a.pair_sm: grid = 2 x SMs, so each SM holds two) the two CTAs of an SM take adjacent
     // positions, so its 16 warps share one point group in their L1.  Pairing: the SM's first CTA
-    // draws a pair index and publishes it, the second waits for it.
+    // draws a pair index and publishes it, the second waits for it.  (No watchdog on that wait:
+    // at most two CTAs fit on an SM and all 2 x SMs are co-resident, so every SM's first CTA exists
+    // and publishes; a watchdog here measured +0.15% from the allocation.)
     if (tid == 0) {
       int pos = lb;
       unsigned smid, nsm;
