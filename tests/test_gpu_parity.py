@@ -480,6 +480,25 @@ def test_persistent_tracker_bit_identical_to_multilaunch(cfg, tmp_path):
     _assert_vs_oracle(dict(outs["0"]), c, c["pst"], params, f"multi-launch {cfg}")
 
 
+@pytest.mark.parametrize("cfg", ["single", "tiny_bigK"])
+def test_persistent_item_order_bit_identical(cfg, tmp_path):
+    """P2's work order does not change any result (every evaluation term is its own fixed-point
+    integer): the SM-paired static item positions (default) and the plain CTA order
+    (PFT_PAIR_SM=0) give bit-identical outputs.  tiny_bigK (K = 70000: >= 1 static item per warp
+    at 296 CTAs) exercises the static items themselves; the persistent run of the
+    same case is compared with the multi-launch path and the oracle above."""
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "run_track.py")
+    outs = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"{cfg}_pair{mode}.npz")
+        subprocess.check_call([sys.executable, helper, cfg, "1", f], env=dict(os.environ, PFT_PAIR_SM=mode))
+        outs[mode] = np.load(f)
+    for k in ("T", "E", "n", "trace"):
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
+
+
 _ORACLE_CACHE = {}
 
 
